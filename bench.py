@@ -1,0 +1,392 @@
+"""bench.py -- fwd+bwd HBM throughput of the ReGELU2/ReSiLU2 + MS-LN/MS-RMSNorm
+hot path on B200, plus activation bytes saved per layer (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one pass of every SURVEY.md section 8(a) row over one batch:
+norm forward -> activation forward -> activation backward -> norm backward
+(the order a transformer block runs them), on inputs already resident in HBM.
+Each kernel is bracketed by its own CUDA events on the launching stream, and
+L2 is flushed (a 2 x L2 write) before every kernel, outside the events, so no
+kernel reads another's output from L2 (in training the whole network runs in
+between).  value = algorithmic bytes of all ranks / max-over-ranks device time.
+
+Multi-GPU: one process per GPU; every rank processes its own batch of the
+configured shape (weak scaling, data-parallel, no collective on the data path);
+NCCL is used only for the barrier and the max/sum of timings.
+
+--impl reference times the float64 CPU oracle (oracle/, the only reference
+this tier has) on a bounded row sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "fwd+bwd HBM GB/s (fraction of B200 peak) and activation bytes saved per layer"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c4", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# bytes
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(cfg, R):
+    b = synth.ELEM_BYTES[cfg["dtype"]]
+    n = R * cfg["F"]
+    H = cfg["H"]
+    act = 2 * b * n + (n + 3) // 4              # read x, write y, write codes  (= read dy, codes; write dx)
+    return {"norm_fwd": (2 * b * H + 4) * R,   # read x, write y, write rstd
+            "act_fwd": act,
+            "act_bwd": act,
+            "norm_bwd": (3 * b * H + 4) * R}   # read dy, y, rstd; write dx
+
+
+def bytes_saved(cfg, R):
+    b = synth.ELEM_BYTES[cfg["dtype"]]
+    n = R * cfg["F"]
+    act_exact, act_ours = n * b, (n + 3) // 4
+    norm_in_fp32 = R * cfg["H"] * 4             # norms run in fp32 under AMP
+    norm_in_t = R * cfg["H"] * b
+    return {"act": {"exact_bytes": act_exact, "ours_bytes": act_ours, "saved_bytes": act_exact - act_ours,
+                    "ratio": round(act_exact / act_ours, 3)},
+            "norm": {"exact_bytes_fp32_input": norm_in_fp32, "exact_bytes_T_input": norm_in_t,
+                     "ours_bytes": 4 * R, "saved_bytes_fp32_input": norm_in_fp32 - 4 * R,
+                     "note": "y is the next linear layer's saved input (Prop. 5.1 cond. 3), counted there"}}
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML) during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+        for k, bit in names.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.nv:
+            self._stop.set()
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the float64 oracle on a bounded row sample
+# ---------------------------------------------------------------------------
+def oracle_step_sample(cfg, rows, eps):
+    """One oracle pass of the four rows of 8(a) on `rows` rows; returns
+    (seconds, algorithmic bytes, threads)."""
+    import oracle
+    dt = cfg["dtype"]
+    x = synth.to_numpy_storage(synth.act_input(rows, cfg["F"], dt))
+    dy = synth.to_numpy_storage(synth.grad_input(rows, cfg["F"], dt))
+    xn = synth.to_numpy_storage(synth.norm_input(rows, cfg["H"], dt))
+    gn = synth.to_numpy_storage(synth.grad_input(rows, cfg["H"], dt, stream=synth.S_NORM_DY))
+    nf, nb = (oracle.msln_fwd, oracle.msln_bwd) if cfg["norm"] == "ln" else (oracle.msrms_fwd, oracle.msrms_bwd)
+    t0 = time.perf_counter()
+    yn, r = nf(oracle.decode(xn, dt), float(np.float32(eps)))
+    yn_st = oracle.round_to(yn, dt)
+    y, codes = oracle.act_fwd(cfg["act"], oracle.decode(x, dt))
+    oracle.round_to(y, dt)
+    oracle.act_bwd_contract(cfg["act"], codes, dy, dt)
+    dxn = nb(oracle.decode(gn, dt), oracle.decode(yn_st, dt), r.astype(np.float32).astype(np.float64))
+    oracle.round_to(dxn, dt)
+    sec = time.perf_counter() - t0
+    return sec, sum(algorithmic_bytes(cfg, rows).values()), oracle.max_threads()
+
+
+def calibrate_rows(cfg, eps, target_s):
+    """Rows of the workload whose oracle pass costs ~target_s seconds."""
+    rows = 8
+    oracle_step_sample(cfg, rows, eps)                    # load / first-touch
+    while True:
+        sec, _, _ = oracle_step_sample(cfg, rows, eps)
+        if sec >= min(0.5, target_s / 4) or rows >= cfg["R"]:
+            break
+        rows = min(cfg["R"], rows * 4)
+    return max(8, min(cfg["R"], int(rows * target_s / max(sec, 1e-4))))
+
+
+def cpu_baseline(cfg, eps, target_s):
+    rows = calibrate_rows(cfg, eps, target_s)
+    sec, nbytes, threads = oracle_step_sample(cfg, rows, eps)
+    return {"value": round(nbytes / sec / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{rows} of {cfg['R']} rows of {cfg['desc']}: norm fwd+bwd and act fwd+bwd, float64 "
+                      f"oracle incl. storage decode/encode, {sec:.2f} s",
+            "seconds": round(sec, 3), "rows": rows}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = synth.CONFIGS[args.config]
+    # each step is a bounded sample: the whole run costs ~4 x cpu_seconds
+    budget = max(0.2, 4 * args.cpu_seconds / max(1, args.steps + args.warmup))
+    rows = calibrate_rows(cfg, args.eps, budget)
+    for _ in range(args.warmup):
+        oracle_step_sample(cfg, rows, args.eps)
+    secs, nbytes, threads = [], 0, 1
+    for _ in range(args.steps):
+        s, nbytes, threads = oracle_step_sample(cfg, rows, args.eps)
+        secs.append(s)
+    total = sum(secs)
+    value = nbytes * len(secs) / total / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / len(secs), 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_step_sample": rows},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{rows} of {cfg['R']} rows per step"},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_2406_16282_b200 as P
+
+    cfg = synth.CONFIGS[args.config]
+    R, F, H, dt = cfg["R"], cfg["F"], cfg["H"], cfg["dtype"]
+    row0 = rank * R                                    # each rank: its own batch (weak scaling)
+    act_fwd, act_bwd = (P.regelu2_fwd, P.regelu2_bwd) if cfg["act"] == "gelu" else (P.resilu2_fwd, P.resilu2_bwd)
+    norm_fwd, norm_bwd = (P.msln_fwd, P.msln_bwd) if cfg["norm"] == "ln" else (P.msrms_fwd, P.msrms_bwd)
+
+    x = synth.act_input(R, F, dt, row_start=row0, device=dev)
+    dy = synth.grad_input(R, F, dt, row_start=row0, device=dev)
+    xn = synth.norm_input(R, H, dt, row_start=row0, device=dev)
+    gn = synth.grad_input(R, H, dt, row_start=row0, device=dev, stream=synth.S_NORM_DY)
+    y, dx = torch.empty_like(x), torch.empty_like(dy)
+    codes = torch.empty(P.codes_bytes(R * F), dtype=torch.uint8, device=dev)
+    yn, dxn = torch.empty_like(xn), torch.empty_like(gn)
+    rstd = torch.empty(R, dtype=torch.float32, device=dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    kernels = ["norm_fwd", "act_fwd", "act_bwd", "norm_bwd"]
+    launch = {
+        "norm_fwd": lambda: norm_fwd(xn, args.eps, y=yn, rstd=rstd, stream=stream),
+        "act_fwd": lambda: act_fwd(x, y=y, codes=codes, stream=stream),
+        "act_bwd": lambda: act_bwd(dy, codes, dx=dx, stream=stream),
+        "norm_bwd": lambda: norm_bwd(gn, yn, rstd, dx=dxn, stream=stream),
+    }
+
+    def step(evs=None):
+        for i, k in enumerate(kernels):
+            flush.fill_(float(i))                       # evict L2 (outside the events)
+            if evs is not None:
+                evs[2 * i].record(stream)
+            launch[k]()
+            if evs is not None:
+                evs[2 * i + 1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    sampler = ClockSampler(dev.index if os.environ.get("CUDA_VISIBLE_DEVICES") is None else local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for s in range(args.steps):
+        step(events[s])
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+
+    per_kernel = {k: [events[s][2 * i].elapsed_time(events[s][2 * i + 1]) for s in range(args.steps)]
+                  for i, k in enumerate(kernels)}
+    total_ms = sum(sum(v) for v in per_kernel.values())
+    nbytes = algorithmic_bytes(cfg, R)
+    step_bytes = sum(nbytes.values())
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = step_bytes * world * args.steps / (max_ms / 1e3) / 1e9
+
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+
+    kern = {}
+    for k in kernels:
+        avg = sum(per_kernel[k]) / len(per_kernel[k])
+        gbs = nbytes[k] / (avg / 1e3) / 1e9
+        kern[k] = {"us": round(avg * 1e3, 2), "us_p10": round(1e3 * float(np.percentile(per_kernel[k], 10)), 2),
+                   "us_p90": round(1e3 * float(np.percentile(per_kernel[k], 90)), 2),
+                   "bytes": nbytes[k], "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
+                   "frac_of_8TBs": round(gbs / NOMINAL_HBM_GBS, 4),
+                   "share": round(sum(per_kernel[k]) / total_ms, 4)}
+    dom = max(kernels, key=lambda k: kern[k]["us"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath)).get(args.config, {})
+        traffic = tr.get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GB/s"], "peak": peak, "unit": "GB/s",
+                "frac": kern[dom]["frac"], "traffic": traffic, "algorithmic_bytes": nbytes[dom],
+                "peak_source": peak_src, "frac_of_8TBs": kern[dom]["frac_of_8TBs"]}
+
+    # e2e through the public API with host buffers: H2D inputs, 4 kernels, D2H results
+    e2e = None
+    if args.e2e_steps > 0:
+        hx = x.cpu().pin_memory()
+        hdy = dy.cpu().pin_memory()
+        hxn = xn.cpu().pin_memory()
+        hgn = gn.cpu().pin_memory()
+        outs = [y, codes, dx, yn, rstd, dxn]
+        houts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+        h2d = sum(t.numel() * t.element_size() for t in (hx, hdy, hxn, hgn))
+        d2h = sum(t.numel() * t.element_size() for t in houts)
+
+        def e2e_step():
+            x.copy_(hx, non_blocking=True)
+            dy.copy_(hdy, non_blocking=True)
+            xn.copy_(hxn, non_blocking=True)
+            gn.copy_(hgn, non_blocking=True)
+            for k in kernels:
+                launch[k]()
+            for o, h in zip(outs, houts):
+                h.copy_(o, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": round(step_bytes * world * args.e2e_steps / (te.item() / 1e3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(te.item() / args.e2e_steps, 3),
+               "path": "pinned host -> H2D -> C-ABI kernels -> D2H pinned host, one stream"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.eps, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_gpu": R, "act_cols": F,
+                       "norm_cols": H, "act": cfg["act"], "norm": cfg["norm"], "eps": args.eps,
+                       "step": "norm_fwd, act_fwd, act_bwd, norm_bwd",
+                       "l2": "flushed before every kernel (write of 2x L2), outside the CUDA events",
+                       "parallelism": f"dp{world} (rows per rank, no data-path collective)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
+            "fraction_of_measured_peak": round(value / world / peak, 4),
+            "fraction_of_8TBs": round(value / world / NOMINAL_HBM_GBS, 4),
+            "elements_per_s": round((R * F * 2 + R * H * 2) * world * args.steps / (max_ms / 1e3), 1),
+            "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,158 @@
+/*
+ * lmbp.h -- C ABI of the B200 (sm_100a) hot path of Approx-BP and
+ * Memory-Sharing BP (arXiv 2406.16282, "Reducing Fine-Tuning Memory Overhead
+ * by Approximate and Memory-Sharing Backpropagation").
+ *
+ * Citations: P:L<n> = reference PAPER.md line n (section / equation /
+ * algorithm beside it); S:L<n> = reference SPEC.md line n.  DESIGN.md lists
+ * every reading (R1..) of the paper that these contracts rely on.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ * ---------------------------------------------------------------------------
+ * Memory.  Every tensor pointer is a DEVICE pointer on the current CUDA
+ *   device.  The caller owns all memory; the library never allocates, frees
+ *   or synchronises.  Tensors are contiguous row-major [rows, cols]
+ *   (row stride = cols elements).  All work is enqueued on `stream`
+ *   (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ * Types.  x / y / dy / dx share `dtype` (LMBP_F32 / LMBP_BF16 / LMBP_F16);
+ *   arithmetic is binary32; conversions round to nearest even; no
+ *   flush-to-zero of stored values.  `rstd` is always binary32.
+ * Packed codes (activation kernels).  n = rows * cols elements are processed
+ *   as one flat sequence; element j's 2-bit segment code is stored in byte
+ *   j >> 2 at bits 2*(j & 3) (LSB first); the buffer holds
+ *   exactly lmbp_codes_bytes(n) = ceil(n / 4) bytes and the unused high bits of
+ *   the last byte are written as 0.
+ * Alignment.  The vector path needs 16-byte aligned tensor pointers (and a
+ *   2-byte aligned `codes` for 16-bit dtypes).  Anything else runs a scalar
+ *   path with bitwise-identical activation results; misalignment is never an
+ *   error.
+ * Aliasing.  Exact aliasing y == x (forward) or dx == dy (backward) is
+ *   allowed: every element / row is read before it is written.  Partial
+ *   overlap is undefined.
+ * Errors.  Arguments are validated synchronously and a status is returned:
+ *   rows < 0, cols <= 0 or rows*cols overflowing int64 -> LMBP_ERR_SHAPE;
+ *   a NULL tensor pointer with rows > 0 -> LMBP_ERR_NULLPTR; unknown dtype ->
+ *   LMBP_ERR_DTYPE; eps not finite or <= 0 -> LMBP_ERR_EPS; a failed launch
+ *   (cudaGetLastError) -> LMBP_ERR_CUDA.  rows == 0 is a no-op returning
+ *   LMBP_OK.  Faults during asynchronous execution surface at the caller's
+ *   next synchronisation, as usual in CUDA.  Nothing is printed, no C++
+ *   exception crosses the ABI.
+ * State.  No global mutable state (constants only): reentrant across host
+ *   threads, streams and devices.  Deterministic: no atomics, fixed
+ *   reduction order, so results are bitwise identical run to run.
+ */
+#ifndef LMBP_H_
+#define LMBP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LMBP_API __attribute__((visibility("default")))
+#else
+#define LMBP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { LMBP_F32 = 0, LMBP_BF16 = 1, LMBP_F16 = 2 } lmbp_dtype;
+
+typedef enum {
+  LMBP_OK = 0,
+  LMBP_ERR_NULLPTR = 1,
+  LMBP_ERR_SHAPE = 2,
+  LMBP_ERR_DTYPE = 3,
+  LMBP_ERR_EPS = 4,
+  LMBP_ERR_CUDA = 5,
+  LMBP_ERR_KIND = 6
+} lmbp_status;
+
+typedef enum { LMBP_GELU = 0, LMBP_SILU = 1 } lmbp_act_kind;
+
+/* ceil(n / 4): bytes of packed 2-bit codes for n elements.
+ * Returns 0 for n <= 0. */
+LMBP_API size_t lmbp_codes_bytes(int64_t n);
+
+/* Static, NUL-terminated description of a status code. */
+LMBP_API const char *lmbp_status_string(int status);
+
+/* Library version string, e.g. "lmbp 0.1.0 sm_100a". */
+LMBP_API const char *lmbp_version(void);
+
+/* Host-side copy of the binary32 step table the kernels use for `kind`
+ * (LMBP_GELU / LMBP_SILU): thresholds[3] and levels[4].  thresholds[i] is the
+ * largest binary32 value <= c_i (round toward -inf, reading R2), so
+ * that for every fp32/bf16/fp16 input `x > thresholds[i]` <=> `x > c_i`
+ * exactly; levels = RN32(0, a1, a1 + a2, 1) (reading R5).  c, a from
+ * P:L1062-1063 (GELU) and P:L1139-1140 (SiLU).  No device access.
+ * Returns LMBP_ERR_NULLPTR / LMBP_ERR_KIND on bad arguments. */
+LMBP_API int lmbp_step_table(int kind, float *thresholds, float *levels);
+
+/* ---------------------------------------------------------------------------
+ * ReGELU2 / ReSiLU2 (Sec. 4.2; App. E)
+ * ---------------------------------------------------------------------------
+ * Forward ("keeps the same primitive function"):
+ *   y[j]  = GELU(x[j]) = x/2 (1 + erf(x/sqrt2))
+ *        or SiLU(x[j]) = x / (1 + e^{-x})
+ *   code[j] = #{i : x[j] > c_i}, c = the published thresholds (P:L1063 /
+ *        P:L1140); strict '>' so a kink takes the lower segment;
+ *        NaN -> code 0.  The code is taken from x as stored in
+ *        `dtype` (reading R3).
+ *   Only `codes` (ceil(n/4) bytes) needs to be kept for backward.
+ *   x: [rows, cols] input; y: [rows, cols] output (may equal x);
+ *   codes: lmbp_codes_bytes(rows*cols) bytes, written in full.
+ * Backward (Prop. 4.1; the derivative of Eq. 14 is the 4-segment
+ *   step function with levels s = (0, a1, a1 + a2, 1)):
+ *   dx[j] = dy[j] * s[code[j]], computed as RN_dtype(RN32(dy * RN32(s)))
+ *   (reading R5; for bf16/fp16 this equals one rounding of the exact product).
+ *   dy: [rows, cols]; codes: as written by the matching *_fwd; dx: [rows,
+ *   cols] output (may equal dy). */
+LMBP_API int regelu2_fwd(const void *x, void *y, uint8_t *codes, int64_t rows, int64_t cols,
+                int dtype, void *stream);
+LMBP_API int regelu2_bwd(const void *dy, const uint8_t *codes, void *dx, int64_t rows, int64_t cols,
+                int dtype, void *stream);
+LMBP_API int resilu2_fwd(const void *x, void *y, uint8_t *codes, int64_t rows, int64_t cols,
+                int dtype, void *stream);
+LMBP_API int resilu2_bwd(const void *dy, const uint8_t *codes, void *dx, int64_t rows, int64_t cols,
+                int dtype, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * MS-LN (Alg. 1; Alg. 2, App. F)
+ * ---------------------------------------------------------------------------
+ * The affine (alpha, beta) is merged into the next linear layer,
+ * so the layer is parameter-free and its output y is the next linear layer's
+ * saved input (Prop. 5.1).  Per row of p = cols elements:
+ * Forward:  mu = (1/p) sum x;  var = (1/p) sum (x - mu)^2   (biased)
+ *           rstd = 1 / sqrt(var + eps);  y = (x - mu) * rstd
+ *           x: [rows, cols]; y: [rows, cols] output (may equal x);
+ *           rstd: [rows] binary32 output (the paper saves sigma = 1/rstd,
+ *           P:L1246; reading R9).  eps: finite, > 0 (1e-6 or 1e-8).
+ * Backward: dx = rstd * (dy - mean(dy) - y * mean(dy * y))   (Alg. 2)
+ *           from (dy, y, rstd) only -- x is never read.
+ *           dy, y: [rows, cols]; rstd: [rows]; dx: [rows, cols] output (may
+ *           equal dy).
+ * ------------------------------------------------------------------------- */
+LMBP_API int msln_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+             int dtype, void *stream);
+LMBP_API int msln_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+             int64_t cols, int dtype, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * MS-RMSNorm (Alg. 3, App. F): as MS-LN with H = I, beta = 0.
+ * Forward:  rstd = 1 / sqrt((1/p) sum x^2 + eps);  y = x * rstd
+ * Backward: dx = rstd * (dy - y * mean(dy * y))
+ * Arguments as msln_*.
+ * ------------------------------------------------------------------------- */
+LMBP_API int msrms_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+              int dtype, void *stream);
+LMBP_API int msrms_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+              int64_t cols, int dtype, void *stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* LMBP_H_ */

@@ -1,0 +1,138 @@
+// abi.cu -- the extern "C" boundary declared in include/lmbp.h.
+// Synchronous argument validation, dtype dispatch, status codes.  No
+// allocation, no synchronisation, nothing printed, no exceptions escape.
+#include <cmath>
+#include <cstring>
+
+#include "../../include/lmbp.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbp {
+
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  return n;
+}
+
+static int check_shape(int64_t rows, int64_t cols) {
+  if (rows < 0 || cols <= 0) return LMBP_ERR_SHAPE;
+  if (rows > 0 && cols > INT64_MAX / rows) return LMBP_ERR_SHAPE;
+  return LMBP_OK;
+}
+
+static int check_dtype(int dtype) {
+  return (dtype == LMBP_F32 || dtype == LMBP_BF16 || dtype == LMBP_F16) ? LMBP_OK : LMBP_ERR_DTYPE;
+}
+
+static int status_of(cudaError_t e) { return e == cudaSuccess ? LMBP_OK : LMBP_ERR_CUDA; }
+
+static int act_fwd_entry(int kind, const void *x, void *y, uint8_t *codes, int64_t rows, int64_t cols, int dtype,
+                         void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!x || !y || !codes) return LMBP_ERR_NULLPTR;
+  return status_of(act_fwd(kind, dtype, x, y, codes, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
+static int act_bwd_entry(int kind, const void *dy, const uint8_t *codes, void *dx, int64_t rows, int64_t cols,
+                         int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!dy || !dx || !codes) return LMBP_ERR_NULLPTR;
+  return status_of(act_bwd(kind, dtype, dy, codes, dx, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
+static int norm_fwd_entry(int kind, const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                          int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (!(eps > 0.0f) || !std::isfinite(eps)) return LMBP_ERR_EPS;
+  if (rows == 0) return LMBP_OK;
+  if (!x || !y || !rstd) return LMBP_ERR_NULLPTR;
+  return status_of(norm_fwd(kind, dtype, x, y, rstd, rows, cols, eps, static_cast<cudaStream_t>(stream)));
+}
+
+static int norm_bwd_entry(int kind, const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+                          int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!dy || !y || !rstd || !dx) return LMBP_ERR_NULLPTR;
+  return status_of(norm_bwd(kind, dtype, dy, y, rstd, dx, rows, cols, static_cast<cudaStream_t>(stream)));
+}
+
+}  // namespace lmbp
+
+extern "C" {
+
+size_t lmbp_codes_bytes(int64_t n) { return n <= 0 ? 0 : (size_t)((n + 3) / 4); }
+
+const char *lmbp_status_string(int status) {
+  switch (status) {
+    case LMBP_OK: return "LMBP_OK";
+    case LMBP_ERR_NULLPTR: return "LMBP_ERR_NULLPTR: a required pointer is NULL";
+    case LMBP_ERR_SHAPE: return "LMBP_ERR_SHAPE: rows < 0, cols <= 0 or rows*cols overflows int64";
+    case LMBP_ERR_DTYPE: return "LMBP_ERR_DTYPE: dtype is not LMBP_F32, LMBP_BF16 or LMBP_F16";
+    case LMBP_ERR_EPS: return "LMBP_ERR_EPS: eps must be finite and > 0";
+    case LMBP_ERR_CUDA: return "LMBP_ERR_CUDA: kernel launch failed (cudaGetLastError)";
+    case LMBP_ERR_KIND: return "LMBP_ERR_KIND: unknown activation kind";
+    default: return "LMBP: unknown status";
+  }
+}
+
+const char *lmbp_version(void) { return "lmbp 0.1.0 sm_100a"; }
+
+int lmbp_step_table(int kind, float *thresholds, float *levels) {
+  if (!thresholds || !levels) return LMBP_ERR_NULLPTR;
+  const uint32_t *t, *l;
+  if (kind == LMBP_GELU) {
+    t = lmbp::kGELU_THR_F32;
+    l = lmbp::kGELU_LVL_F32;
+  } else if (kind == LMBP_SILU) {
+    t = lmbp::kSILU_THR_F32;
+    l = lmbp::kSILU_LVL_F32;
+  } else {
+    return LMBP_ERR_KIND;
+  }
+  std::memcpy(thresholds, t, 3 * sizeof(float));
+  std::memcpy(levels, l, 4 * sizeof(float));
+  return LMBP_OK;
+}
+
+int regelu2_fwd(const void *x, void *y, uint8_t *codes, int64_t rows, int64_t cols, int dtype, void *stream) {
+  return lmbp::act_fwd_entry(lmbp::kActGelu, x, y, codes, rows, cols, dtype, stream);
+}
+int regelu2_bwd(const void *dy, const uint8_t *codes, void *dx, int64_t rows, int64_t cols, int dtype, void *stream) {
+  return lmbp::act_bwd_entry(lmbp::kActGelu, dy, codes, dx, rows, cols, dtype, stream);
+}
+int resilu2_fwd(const void *x, void *y, uint8_t *codes, int64_t rows, int64_t cols, int dtype, void *stream) {
+  return lmbp::act_fwd_entry(lmbp::kActSilu, x, y, codes, rows, cols, dtype, stream);
+}
+int resilu2_bwd(const void *dy, const uint8_t *codes, void *dx, int64_t rows, int64_t cols, int dtype, void *stream) {
+  return lmbp::act_bwd_entry(lmbp::kActSilu, dy, codes, dx, rows, cols, dtype, stream);
+}
+int msln_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps, int dtype, void *stream) {
+  return lmbp::norm_fwd_entry(lmbp::kNormLN, x, y, rstd, rows, cols, eps, dtype, stream);
+}
+int msln_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows, int64_t cols, int dtype,
+             void *stream) {
+  return lmbp::norm_bwd_entry(lmbp::kNormLN, dy, y, rstd, dx, rows, cols, dtype, stream);
+}
+int msrms_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps, int dtype, void *stream) {
+  return lmbp::norm_fwd_entry(lmbp::kNormRMS, x, y, rstd, rows, cols, eps, dtype, stream);
+}
+int msrms_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows, int64_t cols, int dtype,
+              void *stream) {
+  return lmbp::norm_bwd_entry(lmbp::kNormRMS, dy, y, rstd, dx, rows, cols, dtype, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+// act.cu -- ReGELU2 / ReSiLU2 forward and backward kernels (sm_100a).
+//
+// Method (arXiv 2406.16282, Sec. 4.2; App. E):
+//   forward : y = GELU(x) or SiLU(x), unchanged;
+//             code = #{i : x > c_i}, 2 bits per element, 4 per byte.
+//   backward: dx = dy * s[code], s = (0, a1, a1 + a2, 1) -- the derivative of
+//             the ReLU combination of Eq. 14.
+//
+// B200 design:
+//   * HBM-bound streaming: 16-byte vector loads/stores, lane-interleaved so
+//     every warp instruction touches 512 contiguous bytes; U vectors per thread
+//     in flight; grid = SMs x resident CTAs, grid-stride over tiles.
+//   * codes: one 16-bit word per 8 bf16/fp16 elements (one byte per 4 fp32),
+//     stored by the lane that owns the 16-byte vector -> 64 (32) contiguous
+//     bytes per warp store.  16-bit types compute codes with packed x2
+//     compares (HSET2) and a bit-interleave trick, no per-element shifts.
+//   * GELU is evaluated branch-free as max(x,0) - |x| e^{-x^2/2} G(|x|),
+//     G(u) = Phi(-u) e^{u^2/2} ~= t P7(t), t = 1/(1 + k u): 2 MUFU + ~16 FMA-pipe
+//     ops per element; SiLU as max(x,0) - u e^{-u} / (1 + e^{-u}) with the
+//     exponential split e^{-u} = (e^{-u/2})^2 so products underflow gradually.
+//     fp32 outputs add an exact split of the exponent argument ("precise").
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbp {
+
+template <int A> struct Tab;
+template <> struct Tab<kActGelu> {
+  static constexpr uint32_t t0 = kGELU_THR_F32[0], t1 = kGELU_THR_F32[1], t2 = kGELU_THR_F32[2];
+  static constexpr uint16_t b0 = kGELU_THR_BF16[0], b1 = kGELU_THR_BF16[1], b2 = kGELU_THR_BF16[2];
+  static constexpr uint16_t h0 = kGELU_THR_F16[0], h1 = kGELU_THR_F16[1], h2 = kGELU_THR_F16[2];
+  static constexpr uint32_t s1 = kGELU_LVL_F32[1], s2 = kGELU_LVL_F32[2];
+};
+template <> struct Tab<kActSilu> {
+  static constexpr uint32_t t0 = kSILU_THR_F32[0], t1 = kSILU_THR_F32[1], t2 = kSILU_THR_F32[2];
+  static constexpr uint16_t b0 = kSILU_THR_BF16[0], b1 = kSILU_THR_BF16[1], b2 = kSILU_THR_BF16[2];
+  static constexpr uint16_t h0 = kSILU_THR_F16[0], h1 = kSILU_THR_F16[1], h2 = kSILU_THR_F16[2];
+  static constexpr uint32_t s1 = kSILU_LVL_F32[1], s2 = kSILU_LVL_F32[2];
+};
+
+struct GeluPoly {
+  static constexpr uint32_t p0 = kGeluP[0], p1 = kGeluP[1], p2 = kGeluP[2], p3 = kGeluP[3], p4 = kGeluP[4],
+                            p5 = kGeluP[5], p6 = kGeluP[6], p7 = kGeluP[7];
+};
+
+// ---------------------------------------------------------------------------
+// Element math.  Every multiply is an explicit __fmul_rn / fmaf so the
+// vector, scalar and tail paths execute the identical rounding sequence.
+// ---------------------------------------------------------------------------
+template <bool kPrecise>
+__device__ __forceinline__ float exp_neg_half(float v) {  // e^{-v/2}, v >= 0
+  const float KH = __uint_as_float(kExpKH);
+  if constexpr (kPrecise) {
+    const float KL = __uint_as_float(kExpKL);
+    float bh = __fmul_rn(v, KH);
+    float bl = fmaf(v, KH, -bh);  // exact residual of the product
+    bl = fmaf(v, KL, bl);         // + the part of -log2(e)/2 below binary32
+    float e0 = ex2_approx(bh);
+    return fmaf(e0, __fmul_rn(bl, __uint_as_float(kLn2)), e0);  // 2^(bh+bl) ~= 2^bh (1 + bl ln2)
+  } else {
+    return ex2_approx(__fmul_rn(v, KH));
+  }
+}
+
+// GELU(x) = x Phi(x) = max(x,0) - u Phi(-u), u = |x|; Phi(-u) = e^{-u^2/2} G(u).
+template <bool kPrecise>
+__device__ __forceinline__ float gelu_f(float x) {
+  const float u = fabsf(x);
+  const float t = rcp_approx(fmaf(kGeluK, u, 1.0f));
+  float p = __uint_as_float(GeluPoly::p0);  // Horner, degree 7
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p1));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p2));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p3));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p4));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p5));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p6));
+  p = fmaf(p, t, __uint_as_float(GeluPoly::p7));
+  const float q = __fmul_rn(u, __fmul_rn(t, p));  // u G(u)
+  float e;
+  if constexpr (kPrecise) {
+    // e^{-u^2/2} with u^2 split exactly: u^2 = ah + al.
+    const float uc = fminf(u, 16.0f);  // e^{-128} is 0 in binary32 anyway
+    const float ah = __fmul_rn(uc, uc);
+    const float al = fmaf(uc, uc, -ah);
+    const float KH = __uint_as_float(kExpKH), KL = __uint_as_float(kExpKL);
+    const float bh = __fmul_rn(ah, KH);
+    float bl = fmaf(ah, KH, -bh);
+    bl = fmaf(ah, KL, bl);
+    bl = fmaf(al, KH, bl);
+    const float e0 = ex2_approx(bh);
+    e = fmaf(e0, __fmul_rn(bl, __uint_as_float(kLn2)), e0);
+  } else {
+    e = ex2_approx(__fmul_rn(__fmul_rn(u, u), __uint_as_float(kExpKH)));
+  }
+  return fmaf(-q, e, fmaxf(x, 0.0f));
+}
+
+// SiLU(x) = x sigma(x) = max(x,0) - u sigma(-u) = max(x,0) - u e^{-u} / (1 + e^{-u}).
+template <bool kPrecise>
+__device__ __forceinline__ float silu_f(float x) {
+  const float u = fabsf(x);
+  const float eh = exp_neg_half<kPrecise>(u);       // e^{-u/2}, never subnormal for u < 174
+  const float s = rcp_approx(fmaf(eh, eh, 1.0f));   // 1 / (1 + e^{-u})
+  const float q = __fmul_rn(__fmul_rn(__fmul_rn(u, eh), s), eh);
+  return __fsub_rn(fmaxf(x, 0.0f), q);
+}
+
+template <int A, bool kPrecise>
+__device__ __forceinline__ float act_f(float x) {
+  if constexpr (A == kActGelu) return gelu_f<kPrecise>(x);
+  else return silu_f<kPrecise>(x);
+}
+
+// Scalar code: exact for any fp32/bf16/fp16 input (thresholds rounded down).
+template <int A>
+__device__ __forceinline__ uint32_t code_f32(float x) {
+  return (uint32_t)(x > __uint_as_float(Tab<A>::t0)) + (uint32_t)(x > __uint_as_float(Tab<A>::t1)) +
+         (uint32_t)(x > __uint_as_float(Tab<A>::t2));
+}
+
+// From three nested compare masks (m1 >= m2 >= m3 since c1 < c2 < c3):
+// code = m1 + m2 + m3 -> bit0 = m1 ^ m2 ^ m3, bit1 = m2.  Interleave both
+// bits into every 2-bit field of the word, then the caller keeps one field.
+__device__ __forceinline__ uint32_t code_fields(uint32_t m1, uint32_t m2, uint32_t m3) {
+  return ((m1 ^ m2 ^ m3) & 0x55555555u) | (m2 & 0xAAAAAAAAu);
+}
+
+// 4 fp32 elements -> 8 code bits.
+template <int A>
+__device__ __forceinline__ uint32_t codes_vec_f32(const float *f) {
+  const float T0 = __uint_as_float(Tab<A>::t0), T1 = __uint_as_float(Tab<A>::t1),
+              T2 = __uint_as_float(Tab<A>::t2);
+  uint32_t W = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t m1 = f[k] > T0 ? 0xffffffffu : 0u;
+    const uint32_t m2 = f[k] > T1 ? 0xffffffffu : 0u;
+    const uint32_t m3 = f[k] > T2 ? 0xffffffffu : 0u;
+    W |= code_fields(m1, m2, m3) & (0x3u << (2 * k));
+  }
+  return W;
+}
+
+// 8 bf16 / fp16 elements (4 packed pairs) -> 16 code bits.  Pair j holds
+// element 2j in its low half and 2j+1 in its high half; the compare masks are
+// 0xffff per half.  Element 2j's field is taken from bits 4j..4j+1, element
+// 2j+1's from bits 16+4j+2..16+4j+3 and folded down by the final shift.
+template <typename T, int A>
+__device__ __forceinline__ uint32_t codes_vec_16(const uint4 &r) {
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  uint32_t W = 0;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const __nv_bfloat162 T0 = __halves2bfloat162(__ushort_as_bfloat16(Tab<A>::b0), __ushort_as_bfloat16(Tab<A>::b0));
+    const __nv_bfloat162 T1 = __halves2bfloat162(__ushort_as_bfloat16(Tab<A>::b1), __ushort_as_bfloat16(Tab<A>::b1));
+    const __nv_bfloat162 T2 = __halves2bfloat162(__ushort_as_bfloat16(Tab<A>::b2), __ushort_as_bfloat16(Tab<A>::b2));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162 *>(&w[j]);
+      const uint32_t z = code_fields(__hgt2_mask(v, T0), __hgt2_mask(v, T1), __hgt2_mask(v, T2));
+      W |= z & ((0x3u << (4 * j)) | (0x3u << (18 + 4 * j)));
+    }
+  } else {
+    const __half2 T0 = __halves2half2(__ushort_as_half(Tab<A>::h0), __ushort_as_half(Tab<A>::h0));
+    const __half2 T1 = __halves2half2(__ushort_as_half(Tab<A>::h1), __ushort_as_half(Tab<A>::h1));
+    const __half2 T2 = __halves2half2(__ushort_as_half(Tab<A>::h2), __ushort_as_half(Tab<A>::h2));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __half2 v = *reinterpret_cast<const __half2 *>(&w[j]);
+      const uint32_t z = code_fields(__hgt2_mask(v, T0), __hgt2_mask(v, T1), __hgt2_mask(v, T2));
+      W |= z & ((0x3u << (4 * j)) | (0x3u << (18 + 4 * j)));
+    }
+  }
+  return (W | (W >> 16)) & 0xffffu;
+}
+
+template <typename T> using CodeWord = typename std::conditional<Traits<T>::kVec == 8, uint16_t, uint8_t>::type;
+
+// Level s[c] for a 2-bit code (s0 = 0, s3 = 1 exactly).
+template <int A>
+__device__ __forceinline__ float level(uint32_t c) {
+  const float lo = (c & 1u) ? __uint_as_float(Tab<A>::s1) : 0.0f;
+  const float hi = (c & 1u) ? 1.0f : __uint_as_float(Tab<A>::s2);
+  return (c & 2u) ? hi : lo;
+}
+
+// Scalar fp32/bf16/fp16 tail: elements [j0, n), j0 a multiple of 4.
+template <typename T, int A, bool kPrecise>
+__device__ void act_fwd_tail(const T *x, T *y, uint8_t *codes, int64_t j0, int64_t n) {
+  for (int64_t b = j0 >> 2; 4 * b < n; ++b) {
+    uint32_t byte = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = 4 * b + k;
+      if (j >= n) break;
+      const float f = to_f32<T>(x[j]);
+      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+      byte |= code_f32<A>(f) << (2 * k);
+    }
+    codes[b] = (uint8_t)byte;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward, vector path.
+// ---------------------------------------------------------------------------
+template <typename T, int A, bool kPrecise, int U>
+__global__ void __launch_bounds__(256) act_fwd_vec(const uint4 *x, uint4 *y, uint8_t *codes, int64_t nvec,
+                                                   int64_t n) {
+  constexpr int kVec = Traits<T>::kVec;
+  CodeWord<T> *cw = reinterpret_cast<CodeWord<T> *>(codes);
+  const int64_t tile = (int64_t)blockDim.x * U;
+  for (int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x; base < nvec; base += (int64_t)gridDim.x * tile) {
+    uint4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      if (i < nvec) v[j] = ld_stream(x + i);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      if (i < nvec) {
+        float f[kVec];
+        Vec<T>::unpack(v[j], f);
+        uint32_t c;
+        if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
+        else c = codes_vec_16<T, A>(v[j]);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) f[k] = act_f<A, kPrecise>(f[k]);
+        st_stream(y + i, Vec<T>::pack(f));
+        cw[i] = (CodeWord<T>)c;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nvec * kVec < n)
+    act_fwd_tail<T, A, kPrecise>(reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y), codes, nvec * kVec, n);
+}
+
+// Forward, scalar path (any alignment): one code byte (4 elements) per thread.
+template <typename T, int A, bool kPrecise>
+__global__ void __launch_bounds__(256) act_fwd_scalar(const T *x, T *y, uint8_t *codes, int64_t n) {
+  const int64_t nbytes = (n + 3) >> 2;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t byte = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = 4 * b + k;
+      if (j < n) {
+        const float f = to_f32<T>(x[j]);
+        y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+        byte |= code_f32<A>(f) << (2 * k);
+      }
+    }
+    codes[b] = (uint8_t)byte;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward.
+// ---------------------------------------------------------------------------
+template <typename T, int A, int U>
+__global__ void __launch_bounds__(256) act_bwd_vec(const uint4 *dy, const uint8_t *codes, uint4 *dx, int64_t nvec,
+                                                   int64_t n) {
+  constexpr int kVec = Traits<T>::kVec;
+  const CodeWord<T> *cw = reinterpret_cast<const CodeWord<T> *>(codes);
+  const int64_t tile = (int64_t)blockDim.x * U;
+  for (int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x; base < nvec; base += (int64_t)gridDim.x * tile) {
+    uint4 v[U];
+    uint32_t c[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      if (i < nvec) {
+        v[j] = ld_stream(dy + i);
+        c[j] = cw[i];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      if (i < nvec) {
+        float f[kVec];
+        Vec<T>::unpack(v[j], f);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) f[k] = __fmul_rn(f[k], level<A>((c[j] >> (2 * k)) & 3u));
+        st_stream(dx + i, Vec<T>::pack(f));
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const T *dys = reinterpret_cast<const T *>(dy);
+    T *dxs = reinterpret_cast<T *>(dx);
+    for (int64_t j = nvec * kVec; j < n; ++j) {
+      const uint32_t cj = (codes[j >> 2] >> (2 * (j & 3))) & 3u;
+      dxs[j] = from_f32<T>(__fmul_rn(to_f32<T>(dys[j]), level<A>(cj)));
+    }
+  }
+}
+
+template <typename T, int A>
+__global__ void __launch_bounds__(256) act_bwd_scalar(const T *dy, const uint8_t *codes, T *dx, int64_t n) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t cj = (codes[j >> 2] >> (2 * (j & 3))) & 3u;
+    dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), level<A>(cj)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+// ---------------------------------------------------------------------------
+template <typename K>
+static int occupancy(K kernel, int threads) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  return b;
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int kActThreads = 256;
+constexpr int kActUnroll = 4;
+
+template <typename T, int A>
+static cudaError_t act_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, cudaStream_t s) {
+  constexpr int kVec = Traits<T>::kVec;
+  constexpr bool kPrecise = std::is_same<T, float>::value;
+  const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
+                       (kVec == 4 || (uintptr_t)codes % 2 == 0);
+  const int sms = sm_count();
+  if (aligned) {
+    auto kern = act_fwd_vec<T, A, kPrecise, kActUnroll>;
+    static const int occ = occupancy(kern, kActThreads);
+    const int64_t nvec = n / kVec;
+    const int64_t want = cdiv(nvec, (int64_t)kActThreads * kActUnroll);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
+    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const uint4 *>(x), reinterpret_cast<uint4 *>(y), codes,
+                                      nvec, n);
+  } else {
+    auto kern = act_fwd_scalar<T, A, kPrecise>;
+    static const int occ = occupancy(kern, kActThreads);
+    const int64_t want = cdiv(cdiv(n, 4), kActThreads);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
+    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y), codes, n);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, int A>
+static cudaError_t act_bwd_t(const void *dy, const uint8_t *codes, void *dx, int64_t n, cudaStream_t s) {
+  constexpr int kVec = Traits<T>::kVec;
+  const bool aligned = ((uintptr_t)dy % 16 == 0) && ((uintptr_t)dx % 16 == 0) &&
+                       (kVec == 4 || (uintptr_t)codes % 2 == 0);
+  const int sms = sm_count();
+  if (aligned) {
+    auto kern = act_bwd_vec<T, A, kActUnroll>;
+    static const int occ = occupancy(kern, kActThreads);
+    const int64_t nvec = n / kVec;
+    const int64_t want = cdiv(nvec, (int64_t)kActThreads * kActUnroll);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
+    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const uint4 *>(dy), codes, reinterpret_cast<uint4 *>(dx),
+                                      nvec, n);
+  } else {
+    auto kern = act_bwd_scalar<T, A>;
+    static const int occ = occupancy(kern, kActThreads);
+    const int64_t want = cdiv(n, kActThreads);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
+    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const T *>(dy), codes, reinterpret_cast<T *>(dx), n);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t act_fwd(int kind, int dtype, const void *x, void *y, uint8_t *codes, int64_t n, cudaStream_t s) {
+  if (kind == kActGelu) {
+    if (dtype == 0) return act_fwd_t<float, kActGelu>(x, y, codes, n, s);
+    if (dtype == 1) return act_fwd_t<__nv_bfloat16, kActGelu>(x, y, codes, n, s);
+    return act_fwd_t<__half, kActGelu>(x, y, codes, n, s);
+  }
+  if (dtype == 0) return act_fwd_t<float, kActSilu>(x, y, codes, n, s);
+  if (dtype == 1) return act_fwd_t<__nv_bfloat16, kActSilu>(x, y, codes, n, s);
+  return act_fwd_t<__half, kActSilu>(x, y, codes, n, s);
+}
+
+cudaError_t act_bwd(int kind, int dtype, const void *dy, const uint8_t *codes, void *dx, int64_t n, cudaStream_t s) {
+  if (kind == kActGelu) {
+    if (dtype == 0) return act_bwd_t<float, kActGelu>(dy, codes, dx, n, s);
+    if (dtype == 1) return act_bwd_t<__nv_bfloat16, kActGelu>(dy, codes, dx, n, s);
+    return act_bwd_t<__half, kActGelu>(dy, codes, dx, n, s);
+  }
+  if (dtype == 0) return act_bwd_t<float, kActSilu>(dy, codes, dx, n, s);
+  if (dtype == 1) return act_bwd_t<__nv_bfloat16, kActSilu>(dy, codes, dx, n, s);
+  return act_bwd_t<__half, kActSilu>(dy, codes, dx, n, s);
+}
+
+}  // namespace lmbp

@@ -1,0 +1,163 @@
+// common.cuh -- shared device helpers for the lmbp kernels (sm_100a).
+// Product code: nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "constants.cuh"
+
+namespace lmbp {
+
+// ---------------------------------------------------------------------------
+// Storage-type traits.  One 16-byte vector holds kVec elements.
+// ---------------------------------------------------------------------------
+template <typename T> struct Traits;
+template <> struct Traits<float> {
+  static constexpr int kVec = 4;
+};
+template <> struct Traits<__nv_bfloat16> {
+  static constexpr int kVec = 8;
+};
+template <> struct Traits<__half> {
+  static constexpr int kVec = 8;
+};
+
+__device__ __forceinline__ float bits_f32(uint32_t b) { return __uint_as_float(b); }
+
+// ---------------------------------------------------------------------------
+// Global memory: 128-bit streaming loads/stores.  Plain ld.global (no .nc) so
+// exact aliasing (y == x, dx == dy) stays well defined; L1::no_allocate keeps
+// streamed data from displacing anything in L1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Element conversions (round-to-nearest-even, no FTZ).
+// ---------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <> __device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <> __device__ __forceinline__ __half from_f32<__half>(float v) { return __float2half_rn(v); }
+
+// 16-byte vector <-> kVec floats.
+template <typename T> struct Vec;
+
+template <> struct Vec<float> {
+  __device__ __forceinline__ static void unpack(const uint4 &r, float *f) {
+    f[0] = __uint_as_float(r.x);
+    f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z);
+    f[3] = __uint_as_float(r.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float *f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+
+__device__ __forceinline__ void bf2_unpack(uint32_t w, float &lo, float &hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xffff0000u);
+}
+__device__ __forceinline__ uint32_t bf2_pack(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // F2FP.BF16.F32.PACK_AB, RNE
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <> struct Vec<__nv_bfloat16> {
+  __device__ __forceinline__ static void unpack(const uint4 &r, float *f) {
+    bf2_unpack(r.x, f[0], f[1]);
+    bf2_unpack(r.y, f[2], f[3]);
+    bf2_unpack(r.z, f[4], f[5]);
+    bf2_unpack(r.w, f[6], f[7]);
+  }
+  __device__ __forceinline__ static uint4 pack(const float *f) {
+    return make_uint4(bf2_pack(f[0], f[1]), bf2_pack(f[2], f[3]), bf2_pack(f[4], f[5]),
+                      bf2_pack(f[6], f[7]));
+  }
+};
+
+__device__ __forceinline__ void h2_unpack(uint32_t w, float &lo, float &hi) {
+  __half2 h = *reinterpret_cast<__half2 *>(&w);
+  float2 f = __half22float2(h);
+  lo = f.x;
+  hi = f.y;
+}
+__device__ __forceinline__ uint32_t h2_pack(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <> struct Vec<__half> {
+  __device__ __forceinline__ static void unpack(const uint4 &r, float *f) {
+    h2_unpack(r.x, f[0], f[1]);
+    h2_unpack(r.y, f[2], f[3]);
+    h2_unpack(r.z, f[4], f[5]);
+    h2_unpack(r.w, f[6], f[7]);
+  }
+  __device__ __forceinline__ static uint4 pack(const float *f) {
+    return make_uint4(h2_pack(f[0], f[1]), h2_pack(f[2], f[3]), h2_pack(f[4], f[5]),
+                      h2_pack(f[6], f[7]));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// MUFU wrappers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {  // 2^x, FTZ
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {  // 1/x, FTZ
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// Reductions (fixed order -> deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float2 warp_sum2(float2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// Device attribute helpers (host side).
+int sm_count();
+
+}  // namespace lmbp

@@ -1,0 +1,21 @@
+// kernels.h -- internal launch entry points behind the C ABI (abi.cu).
+// Arguments are already validated; every function enqueues on `s` and returns
+// cudaGetLastError().
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lmbp {
+
+enum { kActGelu = 0, kActSilu = 1 };
+enum { kNormLN = 0, kNormRMS = 1 };
+
+cudaError_t act_fwd(int kind, int dtype, const void *x, void *y, uint8_t *codes, int64_t n, cudaStream_t s);
+cudaError_t act_bwd(int kind, int dtype, const void *dy, const uint8_t *codes, void *dx, int64_t n,
+                    cudaStream_t s);
+cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, int64_t rows, int64_t cols,
+                     float eps, cudaStream_t s);
+cudaError_t norm_bwd(int kind, int dtype, const void *dy, const void *y, const float *rstd, void *dx,
+                     int64_t rows, int64_t cols, cudaStream_t s);
+
+}  // namespace lmbp

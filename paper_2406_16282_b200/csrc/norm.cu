@@ -1,0 +1,425 @@
+// norm.cu -- MS-LN / MS-RMSNorm forward and backward kernels (sm_100a).
+//
+// Method (arXiv 2406.16282, Sec. 5.2 Alg. 1; App. F Alg. 2-3,
+// P:L1236-1272).  Per row of p = cols elements:
+//   MS-LN fwd : mu = mean(x); var = mean((x-mu)^2); rstd = 1/sqrt(var+eps);
+//               y = (x - mu) rstd                                    (Alg. 2)
+//   MS-LN bwd : dx = rstd (dy - mean(dy) - y mean(dy y))
+//   MS-RMS fwd: rstd = 1/sqrt(mean(x^2)+eps); y = x rstd             (Alg. 3)
+//   MS-RMS bwd: dx = rstd (dy - y mean(dy y))
+// The affine is merged into the next linear layer, so there are
+// no parameter reads and no dgamma/dbeta column reductions.
+//
+// B200 design: a row is owned by a team of
+// `team` threads (one warp, or one CTA of up to 512 threads); each thread
+// holds V <= 8 lane-interleaved 16-byte vectors of the row in registers, so
+// every byte is read from HBM exactly once (two-pass statistics come from
+// registers).  Reductions: warp shuffles, then (CTA teams) one fixed-order
+// pass over per-warp partials in shared memory -> deterministic.  Persistent
+// grid-stride over rows.  Rows that are misaligned or longer than 8 x 1024
+// vectors (32768 bf16 / 16384 fp32 elements) take a scalar multi-pass path.
+#include <algorithm>
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbp {
+
+template <bool kWarpTeam>
+__device__ __forceinline__ float team_sum(float v, float *buf) {
+  v = warp_sum(v);
+  if constexpr (kWarpTeam) {
+    return v;
+  } else {
+    const int nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float t = 0.0f;
+    for (int w = 0; w < nw; ++w) t += buf[w];
+    return t;
+  }
+}
+
+template <bool kWarpTeam>
+__device__ __forceinline__ float2 team_sum2(float2 v, float2 *buf) {
+  v = warp_sum2(v);
+  if constexpr (kWarpTeam) {
+    return v;
+  } else {
+    const int nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float2 t = make_float2(0.0f, 0.0f);
+    for (int w = 0; w < nw; ++w) {
+      t.x += buf[w].x;
+      t.y += buf[w].y;
+    }
+    return t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward, vector path.
+// ---------------------------------------------------------------------------
+// Warp teams run in 256-thread CTAs (8 rows in flight per CTA); CTA teams have
+// at most 512 threads, so both variants get >= 128 registers per thread.
+template <typename T, int NORM, int V, bool kWarpTeam>
+__global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint4 *x, uint4 *y, float *rstd,
+                                                     int64_t rows, int nvec, int cols, float eps) {
+  constexpr int kVec = Traits<T>::kVec;
+  __shared__ float red[2][32];
+  const int team = kWarpTeam ? 32 : (int)blockDim.x;
+  const int tid = kWarpTeam ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
+  const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
+  const float fcols = (float)cols;
+  int it = 0;
+  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+    const uint4 *xr = x + row * nvec;
+    uint4 raw[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int vi = j * team + tid;
+      if (vi < nvec) raw[j] = ld_stream(xr + vi);
+      else raw[j] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    float mean = 0.0f;
+    float ss = 0.0f;
+    if constexpr (NORM == kNormLN) {
+      float s = 0.0f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        float f[kVec];
+        Vec<T>::unpack(raw[j], f);  // zero-filled slots add 0
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) s += f[k];
+      }
+      mean = __fdiv_rn(team_sum<kWarpTeam>(s, red[0]), fcols);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (j * team + tid < nvec) {
+          float f[kVec];
+          Vec<T>::unpack(raw[j], f);
+#pragma unroll
+          for (int k = 0; k < kVec; ++k) {
+            const float d = __fsub_rn(f[k], mean);
+            ss = fmaf(d, d, ss);
+          }
+        }
+      }
+      ss = team_sum<kWarpTeam>(ss, red[1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        float f[kVec];
+        Vec<T>::unpack(raw[j], f);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) ss = fmaf(f[k], f[k], ss);
+      }
+      ss = team_sum<kWarpTeam>(ss, red[it & 1]);
+    }
+    const float r = rsqrtf(__fadd_rn(__fdiv_rn(ss, fcols), eps));
+    uint4 *yr = y + row * nvec;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int vi = j * team + tid;
+      if (vi < nvec) {
+        float f[kVec];
+        Vec<T>::unpack(raw[j], f);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) f[k] = __fmul_rn(NORM == kNormLN ? __fsub_rn(f[k], mean) : f[k], r);
+        st_stream(yr + vi, Vec<T>::pack(f));
+      }
+    }
+    if (tid == 0) rstd[row] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward, vector path.
+// ---------------------------------------------------------------------------
+template <typename T, int NORM, int V, bool kWarpTeam>
+__global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint4 *dy, const uint4 *__restrict__ y,
+                                                     const float *__restrict__ rstd, uint4 *dx, int64_t rows,
+                                                     int nvec, int cols) {
+  constexpr int kVec = Traits<T>::kVec;
+  __shared__ float2 red[2][32];
+  const int team = kWarpTeam ? 32 : (int)blockDim.x;
+  const int tid = kWarpTeam ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
+  const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
+  const float fcols = (float)cols;
+  int it = 0;
+  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+    const uint4 *gr = dy + row * nvec;
+    const uint4 *yr = y + row * nvec;
+    const float r = rstd[row];
+    uint4 rg[V], ry[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int vi = j * team + tid;
+      if (vi < nvec) {
+        rg[j] = ld_stream(gr + vi);
+        ry[j] = ld_stream(yr + vi);
+      } else {
+        rg[j] = make_uint4(0u, 0u, 0u, 0u);
+        ry[j] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    float2 acc = make_float2(0.0f, 0.0f);  // (sum dy, sum dy*y)
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float g[kVec], h[kVec];
+      Vec<T>::unpack(rg[j], g);
+      Vec<T>::unpack(ry[j], h);
+#pragma unroll
+      for (int k = 0; k < kVec; ++k) {
+        if constexpr (NORM == kNormLN) acc.x += g[k];
+        acc.y = fmaf(g[k], h[k], acc.y);
+      }
+    }
+    acc = team_sum2<kWarpTeam>(acc, red[it & 1]);
+    const float m1 = NORM == kNormLN ? __fdiv_rn(acc.x, fcols) : 0.0f;
+    const float m2 = __fdiv_rn(acc.y, fcols);
+    uint4 *dr = dx + row * nvec;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int vi = j * team + tid;
+      if (vi < nvec) {
+        float g[kVec], h[kVec];
+        Vec<T>::unpack(rg[j], g);
+        Vec<T>::unpack(ry[j], h);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+          const float c = NORM == kNormLN ? __fsub_rn(g[k], m1) : g[k];
+          g[k] = __fmul_rn(r, fmaf(-h[k], m2, c));
+        }
+        st_stream(dr + vi, Vec<T>::pack(g));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scalar multi-pass fallback (any alignment / any length): one CTA per row.
+// ---------------------------------------------------------------------------
+template <typename T, int NORM>
+__global__ void __launch_bounds__(256) norm_fwd_scalar(const T *x, T *y, float *rstd, int64_t rows, int64_t cols,
+                                                       float eps) {
+  __shared__ float red[2][32];
+  const float fcols = (float)cols;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const T *xr = x + row * cols;
+    float mean = 0.0f;
+    if constexpr (NORM == kNormLN) {
+      float s = 0.0f;
+      for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) s += to_f32<T>(xr[i]);
+      mean = __fdiv_rn(team_sum<false>(s, red[0]), fcols);
+    }
+    float ss = 0.0f;
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) {
+      const float d = __fsub_rn(to_f32<T>(xr[i]), mean);
+      ss = fmaf(d, d, ss);
+    }
+    ss = team_sum<false>(ss, red[1]);
+    const float r = rsqrtf(__fadd_rn(__fdiv_rn(ss, fcols), eps));
+    __syncthreads();  // every thread has read x before any y store (y may alias x)
+    T *yr = y + row * cols;
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x)
+      yr[i] = from_f32<T>(__fmul_rn(__fsub_rn(to_f32<T>(xr[i]), mean), r));
+    if (threadIdx.x == 0) rstd[row] = r;
+    __syncthreads();
+  }
+}
+
+template <typename T, int NORM>
+__global__ void __launch_bounds__(256) norm_bwd_scalar(const T *dy, const T *y, const float *rstd, T *dx,
+                                                       int64_t rows, int64_t cols) {
+  __shared__ float2 red[2][32];
+  const float fcols = (float)cols;
+  int it = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
+    const T *gr = dy + row * cols;
+    const T *yr = y + row * cols;
+    float2 acc = make_float2(0.0f, 0.0f);
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) {
+      const float g = to_f32<T>(gr[i]);
+      if constexpr (NORM == kNormLN) acc.x += g;
+      acc.y = fmaf(g, to_f32<T>(yr[i]), acc.y);
+    }
+    acc = team_sum2<false>(acc, red[it & 1]);
+    const float m1 = NORM == kNormLN ? __fdiv_rn(acc.x, fcols) : 0.0f;
+    const float m2 = __fdiv_rn(acc.y, fcols);
+    const float r = rstd[row];
+    __syncthreads();  // dx may alias dy
+    T *dr = dx + row * cols;
+    for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) {
+      const float g = to_f32<T>(gr[i]);
+      const float c = NORM == kNormLN ? __fsub_rn(g, m1) : g;
+      dr[i] = from_f32<T>(__fmul_rn(r, fmaf(-to_f32<T>(yr[i]), m2, c)));
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launch configuration.
+// ---------------------------------------------------------------------------
+struct RowPlan {
+  bool vec;
+  bool warp_team;
+  int team;  // threads per row
+  int V;     // vectors per thread
+  int nvec;  // vectors per row
+};
+
+template <typename T>
+static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void *c) {
+  constexpr int kVec = Traits<T>::kVec;
+  RowPlan p{false, false, 0, 0, 0};
+  const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)c % 16 == 0) &&
+                       (cols % kVec == 0);
+  if (!aligned) return p;
+  const int64_t nvec = cols / kVec;
+  if (nvec > 8 * 512) return p;
+  p.nvec = (int)nvec;
+  if (nvec <= 4 * 32) {  // one warp per row, up to 4 vectors per lane
+    p.warp_team = true;
+    p.team = 32;
+    p.V = (int)((nvec + 31) / 32);
+  } else {
+    const int64_t want = (nvec + 3) / 4;           // aim for 4 vectors per thread
+    int64_t team = ((want + 31) / 32) * 32;
+    if (team > 512) team = 512;
+    p.team = (int)team;
+    p.V = (int)((nvec + team - 1) / team);
+  }
+  p.vec = p.V >= 1 && p.V <= (p.warp_team ? 4 : 8);
+  return p;
+}
+
+// Resident CTAs per SM for (kernel, threads); cached per kernel instantiation
+// and block size (a benign race: every writer stores the same value).
+template <typename K>
+static int occupancy_of(K kernel, int threads) {
+  static int cache[33] = {0};
+  const int slot = threads >> 5;
+  if (slot < 33 && cache[slot] > 0) return cache[slot];
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  if (slot < 33) cache[slot] = b;
+  return b;
+}
+
+template <typename K, typename... Args>
+static void launch_rows(K kernel, int64_t rows, int rows_per_block, int threads, cudaStream_t s, int occ,
+                        Args... args) {
+  const int64_t want = (rows + rows_per_block - 1) / rows_per_block;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
+  kernel<<<grid, threads, 0, s>>>(args...);
+}
+
+template <typename T, int NORM, int V, bool W>
+static void fwd_v(const RowPlan &p, const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                  cudaStream_t s) {
+  auto k = norm_fwd_vec<T, NORM, V, W>;
+  const int threads = W ? 256 : p.team;
+  const int occ = occupancy_of(k, threads);
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, reinterpret_cast<const uint4 *>(x),
+              reinterpret_cast<uint4 *>(y), rstd, rows, p.nvec, (int)cols, eps);
+}
+
+template <typename T, int NORM, int V, bool W>
+static void bwd_v(const RowPlan &p, const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+                  int64_t cols, cudaStream_t s) {
+  auto k = norm_bwd_vec<T, NORM, V, W>;
+  const int threads = W ? 256 : p.team;
+  const int occ = occupancy_of(k, threads);
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, reinterpret_cast<const uint4 *>(dy),
+              reinterpret_cast<const uint4 *>(y), rstd, reinterpret_cast<uint4 *>(dx), rows, p.nvec, (int)cols);
+}
+
+template <typename T, int NORM>
+static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                              cudaStream_t s) {
+  const RowPlan p = plan_rows<T>(cols, x, y, y);
+  if (!p.vec) {
+    auto k = norm_fwd_scalar<T, NORM>;
+    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
+                rstd, rows, cols, eps);
+    return cudaGetLastError();
+  }
+#define LMBP_FWD_CASE(VV)                                                                   \
+  case VV:                                                                                  \
+    if constexpr (VV <= 4) {                                                                \
+      if (p.warp_team) {                                                                    \
+        fwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, x, y, rstd, rows, cols, eps, s);        \
+        break;                                                                              \
+      }                                                                                     \
+    }                                                                                       \
+    fwd_v<T, NORM, VV, false>(p, x, y, rstd, rows, cols, eps, s);                           \
+    break;
+  switch (p.V) {
+    LMBP_FWD_CASE(1) LMBP_FWD_CASE(2) LMBP_FWD_CASE(3) LMBP_FWD_CASE(4)
+    LMBP_FWD_CASE(5) LMBP_FWD_CASE(6) LMBP_FWD_CASE(7) LMBP_FWD_CASE(8)
+    default: break;
+  }
+#undef LMBP_FWD_CASE
+  return cudaGetLastError();
+}
+
+template <typename T, int NORM>
+static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+                              int64_t cols, cudaStream_t s) {
+  const RowPlan p = plan_rows<T>(cols, dy, y, dx);
+  if (!p.vec) {
+    auto k = norm_bwd_scalar<T, NORM>;
+    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(dy),
+                reinterpret_cast<const T *>(y), rstd, reinterpret_cast<T *>(dx), rows, cols);
+    return cudaGetLastError();
+  }
+#define LMBP_BWD_CASE(VV)                                                                   \
+  case VV:                                                                                  \
+    if constexpr (VV <= 4) {                                                                \
+      if (p.warp_team) {                                                                    \
+        bwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, dy, y, rstd, dx, rows, cols, s);        \
+        break;                                                                              \
+      }                                                                                     \
+    }                                                                                       \
+    bwd_v<T, NORM, VV, false>(p, dy, y, rstd, dx, rows, cols, s);                           \
+    break;
+  switch (p.V) {
+    LMBP_BWD_CASE(1) LMBP_BWD_CASE(2) LMBP_BWD_CASE(3) LMBP_BWD_CASE(4)
+    LMBP_BWD_CASE(5) LMBP_BWD_CASE(6) LMBP_BWD_CASE(7) LMBP_BWD_CASE(8)
+    default: break;
+  }
+#undef LMBP_BWD_CASE
+  return cudaGetLastError();
+}
+
+cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                     cudaStream_t s) {
+  if (kind == kNormLN) {
+    if (dtype == 0) return norm_fwd_t<float, kNormLN>(x, y, rstd, rows, cols, eps, s);
+    if (dtype == 1) return norm_fwd_t<__nv_bfloat16, kNormLN>(x, y, rstd, rows, cols, eps, s);
+    return norm_fwd_t<__half, kNormLN>(x, y, rstd, rows, cols, eps, s);
+  }
+  if (dtype == 0) return norm_fwd_t<float, kNormRMS>(x, y, rstd, rows, cols, eps, s);
+  if (dtype == 1) return norm_fwd_t<__nv_bfloat16, kNormRMS>(x, y, rstd, rows, cols, eps, s);
+  return norm_fwd_t<__half, kNormRMS>(x, y, rstd, rows, cols, eps, s);
+}
+
+cudaError_t norm_bwd(int kind, int dtype, const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
+                     int64_t cols, cudaStream_t s) {
+  if (kind == kNormLN) {
+    if (dtype == 0) return norm_bwd_t<float, kNormLN>(dy, y, rstd, dx, rows, cols, s);
+    if (dtype == 1) return norm_bwd_t<__nv_bfloat16, kNormLN>(dy, y, rstd, dx, rows, cols, s);
+    return norm_bwd_t<__half, kNormLN>(dy, y, rstd, dx, rows, cols, s);
+  }
+  if (dtype == 0) return norm_bwd_t<float, kNormRMS>(dy, y, rstd, dx, rows, cols, s);
+  if (dtype == 1) return norm_bwd_t<__nv_bfloat16, kNormRMS>(dy, y, rstd, dx, rows, cols, s);
+  return norm_bwd_t<__half, kNormRMS>(dy, y, rstd, dx, rows, cols, s);
+}
+
+}  // namespace lmbp

@@ -1,0 +1,120 @@
+"""Autograd functions and modules over the C ABI.
+
+* ReGELU2 / ReSiLU2 save only the packed 2-bit codes.
+* MSLayerNorm / MSRMSNorm are affine-free (the affine is merged into the next
+  linear layer) and save (y, rstd): y is the tensor the next
+  linear layer saves anyway, so it is stored once (Prop. 5.1).
+
+``saved_bytes`` measures the activation memory a forward retains for
+backward (the "activation bytes saved per layer" half of the metric, a7),
+deduplicating tensors that share storage.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import ops
+
+
+class ReGELU2Fn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        y, codes = ops.regelu2_fwd(x.contiguous())
+        ctx.save_for_backward(codes)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (codes,) = ctx.saved_tensors
+        return ops.regelu2_bwd(dy.contiguous(), codes)
+
+
+class ReSiLU2Fn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        y, codes = ops.resilu2_fwd(x.contiguous())
+        ctx.save_for_backward(codes)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (codes,) = ctx.saved_tensors
+        return ops.resilu2_bwd(dy.contiguous(), codes)
+
+
+class MSLayerNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, eps):
+        y, rstd = ops.msln_fwd(x.contiguous(), eps)
+        ctx.save_for_backward(y, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        y, rstd = ctx.saved_tensors
+        return ops.msln_bwd(dy.contiguous(), y, rstd), None
+
+
+class MSRMSNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, eps):
+        y, rstd = ops.msrms_fwd(x.contiguous(), eps)
+        ctx.save_for_backward(y, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        y, rstd = ctx.saved_tensors
+        return ops.msrms_bwd(dy.contiguous(), y, rstd), None
+
+
+class ReGELU2(torch.nn.Module):
+    def forward(self, x):
+        return ReGELU2Fn.apply(x)
+
+
+class ReSiLU2(torch.nn.Module):
+    def forward(self, x):
+        return ReSiLU2Fn.apply(x)
+
+
+class MSLayerNorm(torch.nn.Module):
+    """Affine-free LayerNorm whose backward needs only (y, rstd)."""
+
+    def __init__(self, normalized_shape: int, eps: float = 1e-6):
+        super().__init__()
+        self.normalized_shape = int(normalized_shape)
+        self.eps = float(eps)
+
+    def forward(self, x):
+        if x.shape[-1] != self.normalized_shape:
+            raise ValueError("last dimension mismatch")
+        return MSLayerNormFn.apply(x, self.eps)
+
+
+class MSRMSNorm(torch.nn.Module):
+    def __init__(self, normalized_shape: int, eps: float = 1e-6):
+        super().__init__()
+        self.normalized_shape = int(normalized_shape)
+        self.eps = float(eps)
+
+    def forward(self, x):
+        if x.shape[-1] != self.normalized_shape:
+            raise ValueError("last dimension mismatch")
+        return MSRMSNormFn.apply(x, self.eps)
+
+
+def saved_bytes(fn, *inputs) -> int:
+    """Bytes of activation state ``fn(*inputs)`` saves for backward, with
+    tensors that share storage counted once (storage data_ptr)."""
+    seen = {}
+
+    def pack(t):
+        st = t.untyped_storage()
+        seen[(st.data_ptr(), t.device)] = st.nbytes()
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = fn(*inputs)
+    del out
+    return int(sum(seen.values()))

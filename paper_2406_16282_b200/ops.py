@@ -1,0 +1,156 @@
+"""Thin Python binding over the C ABI: same names as include/lmbp.h.
+
+Argument marshalling only -- every step runs in liblmbp.so's CUDA kernels.
+PyTorch supplies device memory and the current stream.  Tensors must be CUDA,
+contiguous, and fp32 / bf16 / fp16; outputs are allocated when not given.
+Activations treat the tensor as one flat sequence (rows = numel / last dim,
+cols = last dim); norms normalise over the last dimension.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+_DT = {torch.float32: _lib.LMBP_F32, torch.bfloat16: _lib.LMBP_BF16, torch.float16: _lib.LMBP_F16}
+
+
+def codes_bytes(n: int) -> int:
+    return int(lib().lmbp_codes_bytes(int(n)))
+
+
+def _dtype(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}; expected float32, bfloat16 or float16") from None
+
+
+def _rc(t: torch.Tensor):
+    if t.dim() == 0:
+        return 1, 1
+    cols = t.shape[-1]
+    return (t.numel() // cols if cols else 0), cols
+
+
+def _need(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _act_fwd(fn: str, x, y, codes, stream):
+    _need(x, "x")
+    y = torch.empty_like(x) if y is None else _need(y, "y")
+    n = x.numel()
+    codes = torch.empty(codes_bytes(n), dtype=torch.uint8, device=x.device) if codes is None else _need(codes, "codes")
+    if y.shape != x.shape or y.dtype != x.dtype or codes.numel() != codes_bytes(n):
+        raise ValueError(f"{fn}: shape/dtype mismatch")
+    rows, cols = _rc(x)
+    if n == 0:
+        return y, codes
+    check(fn, getattr(lib(), fn)(x.data_ptr(), y.data_ptr(), codes.data_ptr(), rows, cols, _dtype(x),
+                                 _stream(stream)))
+    return y, codes
+
+
+def _act_bwd(fn: str, dy, codes, dx, stream):
+    _need(dy, "dy")
+    _need(codes, "codes")
+    dx = torch.empty_like(dy) if dx is None else _need(dx, "dx")
+    n = dy.numel()
+    if codes.numel() != codes_bytes(n) or codes.dtype != torch.uint8:
+        raise ValueError(f"{fn}: codes must be uint8[{codes_bytes(n)}] (S:L174)")
+    if dx.shape != dy.shape or dx.dtype != dy.dtype:
+        raise ValueError(f"{fn}: shape/dtype mismatch")
+    rows, cols = _rc(dy)
+    if n == 0:
+        return dx
+    check(fn, getattr(lib(), fn)(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols, _dtype(dy),
+                                 _stream(stream)))
+    return dx
+
+
+def regelu2_fwd(x, y=None, codes=None, stream=None):
+    """ReGELU2 forward: (y = GELU(x), packed 2-bit codes).  lmbp.h regelu2_fwd."""
+    return _act_fwd("regelu2_fwd", x, y, codes, stream)
+
+
+def regelu2_bwd(dy, codes, dx=None, stream=None):
+    """ReGELU2 backward: dx = dy * s[code].  lmbp.h regelu2_bwd."""
+    return _act_bwd("regelu2_bwd", dy, codes, dx, stream)
+
+
+def resilu2_fwd(x, y=None, codes=None, stream=None):
+    """ReSiLU2 forward: (y = SiLU(x), packed 2-bit codes).  lmbp.h resilu2_fwd."""
+    return _act_fwd("resilu2_fwd", x, y, codes, stream)
+
+
+def resilu2_bwd(dy, codes, dx=None, stream=None):
+    """ReSiLU2 backward.  lmbp.h resilu2_bwd."""
+    return _act_bwd("resilu2_bwd", dy, codes, dx, stream)
+
+
+def _norm_fwd(fn, x, eps, y, rstd, stream):
+    _need(x, "x")
+    rows, cols = _rc(x)
+    y = torch.empty_like(x) if y is None else _need(y, "y")
+    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None else _need(rstd, "rstd")
+    if y.shape != x.shape or y.dtype != x.dtype or rstd.numel() != rows or rstd.dtype != torch.float32:
+        raise ValueError(f"{fn}: shape/dtype mismatch")
+    check(fn, getattr(lib(), fn)(x.data_ptr(), y.data_ptr(), rstd.data_ptr(), rows, cols, float(eps), _dtype(x),
+                                 _stream(stream)))
+    return y, rstd
+
+
+def _norm_bwd(fn, dy, y, rstd, dx, stream):
+    _need(dy, "dy")
+    _need(y, "y")
+    _need(rstd, "rstd")
+    rows, cols = _rc(dy)
+    dx = torch.empty_like(dy) if dx is None else _need(dx, "dx")
+    if y.shape != dy.shape or y.dtype != dy.dtype or rstd.numel() != rows or dx.shape != dy.shape \
+            or rstd.dtype != torch.float32 or dx.dtype != dy.dtype:
+        raise ValueError(f"{fn}: token/shape mismatch (S:L266)")
+    check(fn, getattr(lib(), fn)(dy.data_ptr(), y.data_ptr(), rstd.data_ptr(), dx.data_ptr(), rows, cols,
+                                 _dtype(dy), _stream(stream)))
+    return dx
+
+
+def msln_fwd(x, eps=1e-6, y=None, rstd=None, stream=None):
+    """MS-LN forward (Alg. 2): (y, rstd).  lmbp.h msln_fwd."""
+    return _norm_fwd("msln_fwd", x, eps, y, rstd, stream)
+
+
+def msln_bwd(dy, y, rstd, dx=None, stream=None):
+    """MS-LN backward from (dy, y, rstd) only.  lmbp.h msln_bwd."""
+    return _norm_bwd("msln_bwd", dy, y, rstd, dx, stream)
+
+
+def msrms_fwd(x, eps=1e-6, y=None, rstd=None, stream=None):
+    """MS-RMSNorm forward (Alg. 3).  lmbp.h msrms_fwd."""
+    return _norm_fwd("msrms_fwd", x, eps, y, rstd, stream)
+
+
+def msrms_bwd(dy, y, rstd, dx=None, stream=None):
+    """MS-RMSNorm backward.  lmbp.h msrms_bwd."""
+    return _norm_bwd("msrms_bwd", dy, y, rstd, dx, stream)
+
+
+def step_table(kind: str):
+    """The kernels' binary32 (thresholds[3], levels[4]) for 'gelu' / 'silu'."""
+    import ctypes
+    t = (ctypes.c_float * 3)()
+    lv = (ctypes.c_float * 4)()
+    check("lmbp_step_table", lib().lmbp_step_table({"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}[kind],
+                                                   ctypes.addressof(t), ctypes.addressof(lv)))
+    return list(t), list(lv)

@@ -139,3 +139,15 @@ def from_numpy_storage(a, dtype: str) -> torch.Tensor:
     if dtype == "bf16":
         return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16)
     return torch.from_numpy(a.copy())
+
+
+def codes_input(n: int, *, device="cpu", base: int = BASE_SEED) -> torch.Tensor:
+    """Uniformly random packed 2-bit codes for n elements (ceil(n/4) bytes),
+    unused trailing bits zero -- a backward-only parity input."""
+    nbytes = (int(n) + 3) // 4
+    g = torch.Generator(device="cpu")
+    g.manual_seed(_seed(7, 0, base))
+    b = torch.randint(0, 256, (nbytes,), generator=g, dtype=torch.int32).to(torch.uint8)
+    if n % 4 and nbytes:
+        b[-1] &= (1 << (2 * (n % 4))) - 1
+    return b.to(device)

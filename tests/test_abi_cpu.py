@@ -1,0 +1,116 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every
+symbol include/lmbp.h declares, its host-only entry points behave, and
+argument validation returns the documented status codes before any device
+work (no compute calls here)."""
+import ctypes
+import json
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_2406_16282_b200 import _lib, ops
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lmbp.h")
+PAPER = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_constants.json")))
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return re.findall(r"LMBP_API\s+[\w\s\*]+?\b(\w+)\s*\(", src)
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = set(declared_symbols())
+    for n in ("regelu2_fwd", "regelu2_bwd", "resilu2_fwd", "resilu2_bwd", "msln_fwd", "msln_bwd", "msrms_fwd",
+              "msrms_bwd", "lmbp_codes_bytes", "lmbp_status_string", "lmbp_step_table", "lmbp_version"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    assert set(declared_symbols()) == set(_lib.SIGNATURES)
+    assert L.lmbp_version().decode().startswith("lmbp")
+
+
+def test_codes_bytes():
+    L = _lib.lib()
+    for n in (0, 1, 3, 4, 5, 8, 1_210_368, 452_984_832, -5):
+        assert L.lmbp_codes_bytes(n) == (max(n, 0) + 3) // 4
+
+
+@pytest.mark.parametrize("kind", ["gelu", "silu"])
+def test_step_table_is_exact_rounding_of_paper_constants(kind):
+    """thresholds = RD32(c) (reading R2): t < c < next_up(t); levels = RN32(s)."""
+    thr, lv = ops.step_table(kind)
+    for t, cs in zip(thr, PAPER[kind]["c"]):
+        c = Fraction(cs)
+        t32 = np.float32(t)
+        up = np.nextafter(t32, np.float32(np.inf), dtype=np.float32)
+        assert Fraction(float(t32)) < c < Fraction(float(up))
+    a1, a2 = (float(v) for v in PAPER[kind]["a"])
+    want = np.array([0.0, a1, a1 + a2, 1.0]).astype(np.float32)
+    assert np.array_equal(np.array(lv, dtype=np.float32), want)
+
+
+def test_status_strings():
+    for st in range(7):
+        assert _lib.status_string(st).startswith("LMBP")
+    assert "unknown" in _lib.status_string(99)
+
+
+def test_validation_without_device_work():
+    L = _lib.lib()
+    S = _lib
+    fake = ctypes.c_void_p(0x1000)   # never dereferenced: validation fails first
+    for fn in (L.regelu2_fwd, L.resilu2_fwd):
+        assert fn(fake, fake, fake, -1, 4, 0, None) == S.LMBP_ERR_SHAPE
+        assert fn(fake, fake, fake, 2, 0, 0, None) == S.LMBP_ERR_SHAPE
+        assert fn(fake, fake, fake, 2**40, 2**40, 0, None) == S.LMBP_ERR_SHAPE   # int64 overflow
+        assert fn(fake, fake, fake, 2, 4, 7, None) == S.LMBP_ERR_DTYPE
+        assert fn(None, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
+        assert fn(fake, fake, None, 2, 4, 1, None) == S.LMBP_ERR_NULLPTR
+        assert fn(None, None, None, 0, 4, 0, None) == S.LMBP_OK                   # rows == 0: no-op
+    for fn in (L.regelu2_bwd, L.resilu2_bwd):
+        assert fn(fake, fake, fake, -1, 4, 0, None) == S.LMBP_ERR_SHAPE
+        assert fn(fake, None, fake, 2, 4, 2, None) == S.LMBP_ERR_NULLPTR
+        assert fn(fake, fake, fake, 2, 4, -1, None) == S.LMBP_ERR_DTYPE
+    for fn in (L.msln_fwd, L.msrms_fwd):
+        assert fn(fake, fake, fake, 2, 4, 0.0, 0, None) == S.LMBP_ERR_EPS
+        assert fn(fake, fake, fake, 2, 4, -1e-6, 0, None) == S.LMBP_ERR_EPS
+        assert fn(fake, fake, fake, 2, 4, float("nan"), 0, None) == S.LMBP_ERR_EPS
+        assert fn(fake, fake, fake, 2, 4, float("inf"), 0, None) == S.LMBP_ERR_EPS
+        assert fn(fake, fake, None, 2, 4, 1e-6, 0, None) == S.LMBP_ERR_NULLPTR
+        assert fn(fake, fake, fake, 2, -4, 1e-6, 0, None) == S.LMBP_ERR_SHAPE
+        assert fn(fake, fake, fake, 2, 4, 1e-6, 3, None) == S.LMBP_ERR_DTYPE
+        assert fn(None, None, None, 0, 4, 1e-6, 0, None) == S.LMBP_OK
+    for fn in (L.msln_bwd, L.msrms_bwd):
+        assert fn(fake, fake, None, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
+        assert fn(fake, fake, fake, fake, -2, 4, 0, None) == S.LMBP_ERR_SHAPE
+        assert fn(fake, fake, fake, fake, 2, 4, 9, None) == S.LMBP_ERR_DTYPE
+    t = (ctypes.c_float * 4)()
+    assert L.lmbp_step_table(5, ctypes.addressof(t), ctypes.addressof(t)) == S.LMBP_ERR_KIND
+    assert L.lmbp_step_table(0, None, ctypes.addressof(t)) == S.LMBP_ERR_NULLPTR
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    with pytest.raises(ValueError, match="CUDA"):
+        ops.regelu2_fwd(torch.zeros(4))
+    with pytest.raises(ValueError, match="CUDA"):
+        ops.msrms_fwd(torch.zeros(2, 4))
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path never touches oracle/ (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2406_16282_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("oracle/", ""), f
