@@ -42,7 +42,7 @@ METRIC = "fwd+bwd HBM GB/s (fraction of B200 peak) and activation bytes saved pe
 NOMINAL_HBM_GBS = 8000.0
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -53,7 +53,26 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
-    return ap.parse_args()
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs the full config (its own batch); "
+                         "strong: the config's rows are split across ranks")
+    return ap.parse_args(argv)
+
+
+def shard_rows(R: int, world: int, rank: int, scaling: str):
+    """(first global row, rows) this rank processes.  weak: each rank owns a
+    whole batch of R rows (rows [rank*R, (rank+1)*R) of the global stream);
+    strong: the R rows are split into contiguous, near-equal blocks."""
+    if scaling == "weak":
+        return rank * R, R
+    lo = (R * rank) // world
+    hi = (R * (rank + 1)) // world
+    return lo, hi - lo
+
+
+def aggregate(step_bytes_per_rank, ms_per_rank, steps):
+    """Whole-job GB/s: bytes of all ranks / the slowest rank's device time."""
+    return sum(step_bytes_per_rank) * steps / (max(ms_per_rank) / 1e3) / 1e9
 
 
 def dist_env():
@@ -235,8 +254,8 @@ def main():
     import paper_2406_16282_b200 as P
 
     cfg = synth.CONFIGS[args.config]
-    R, F, H, dt = cfg["R"], cfg["F"], cfg["H"], cfg["dtype"]
-    row0 = rank * R                                    # each rank: its own batch (weak scaling)
+    F, H, dt = cfg["F"], cfg["H"], cfg["dtype"]
+    row0, R = shard_rows(cfg["R"], world, rank, args.scaling)
     act_fwd, act_bwd = (P.regelu2_fwd, P.regelu2_bwd) if cfg["act"] == "gelu" else (P.resilu2_fwd, P.resilu2_bwd)
     norm_fwd, norm_bwd = (P.msln_fwd, P.msln_bwd) if cfg["norm"] == "ln" else (P.msrms_fwd, P.msrms_bwd)
 
@@ -291,11 +310,16 @@ def main():
     total_ms = sum(sum(v) for v in per_kernel.values())
     nbytes = algorithmic_bytes(cfg, R)
     step_bytes = sum(nbytes.values())
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, float(step_bytes)], dtype=torch.float64, device=dev)
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = step_bytes * world * args.steps / (max_ms / 1e3) / 1e9
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(parts, t)
+    else:
+        parts = [t]
+    ms_all = [float(p[0]) for p in parts]
+    bytes_all = [float(p[1]) for p in parts]
+    max_ms = max(ms_all)
+    value = aggregate(bytes_all, ms_all, args.steps)
 
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
@@ -356,7 +380,7 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": round(step_bytes * world * args.e2e_steps / (te.item() / 1e3) / 1e9, 2), "unit": "GB/s",
+        e2e = {"value": round(sum(bytes_all) * args.e2e_steps / (te.item() / 1e3) / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(te.item() / args.e2e_steps, 3),
                "path": "pinned host -> H2D -> C-ABI kernels -> D2H pinned host, one stream"}
@@ -369,7 +393,7 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": dt, "data": "synthetic",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_gpu": R, "act_cols": F,
                        "norm_cols": H, "act": cfg["act"], "norm": cfg["norm"], "eps": args.eps,
                        "step": "norm_fwd, act_fwd, act_bwd, norm_bwd",
@@ -379,7 +403,9 @@ def main():
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),
             "fraction_of_8TBs": round(value / world / NOMINAL_HBM_GBS, 4),
-            "elements_per_s": round((R * F * 2 + R * H * 2) * world * args.steps / (max_ms / 1e3), 1),
+            "elements_per_s": round(sum(bytes_all) / step_bytes * (R * F * 2 + R * H * 2) * args.steps
+                                    / (max_ms / 1e3), 1),
+            "per_rank_ms": [round(m, 3) for m in ms_all],
             "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
         }
         print(json.dumps(line), flush=True)

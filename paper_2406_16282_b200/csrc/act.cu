@@ -107,6 +107,57 @@ __device__ __forceinline__ float silu_f(float x) {
   return __fsub_rn(fmaxf(x, 0.0f), q);
 }
 
+// Packed-pair versions on sm_100's f32x2 FMA pipe (FFMA2 / FMUL2): the same
+// IEEE operations in the same order as gelu_f / silu_f, lane by lane, so the
+// results are bitwise identical to the scalar path; half the issue slots for
+// the polynomial and the products.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+template <bool kPrecise>
+__device__ __forceinline__ float2 gelu2_f(float2 x) {
+  if constexpr (kPrecise) {
+    return make_float2(gelu_f<true>(x.x), gelu_f<true>(x.y));
+  } else {
+    const float2 u = make_float2(fabsf(x.x), fabsf(x.y));
+    const float2 d = __ffma2_rn(f2(kGeluK), u, f2(1.0f));
+    const float2 t = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+    float2 p = f2(__uint_as_float(GeluPoly::p0));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p1)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p2)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p3)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p4)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p5)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p6)));
+    p = __ffma2_rn(p, t, f2(__uint_as_float(GeluPoly::p7)));
+    const float2 nu = make_float2(-u.x, -u.y);
+    const float2 nq = __fmul2_rn(nu, __fmul2_rn(t, p));  // -u G(u), exact negation of q
+    const float2 a = __fmul2_rn(__fmul2_rn(u, u), f2(__uint_as_float(kExpKH)));
+    const float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+    return __ffma2_rn(nq, e, make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
+  }
+}
+
+template <bool kPrecise>
+__device__ __forceinline__ float2 silu2_f(float2 x) {
+  if constexpr (kPrecise) {
+    return make_float2(silu_f<true>(x.x), silu_f<true>(x.y));
+  } else {
+    const float2 u = make_float2(fabsf(x.x), fabsf(x.y));
+    const float2 a = __fmul2_rn(u, f2(__uint_as_float(kExpKH)));
+    const float2 eh = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+    const float2 d = __ffma2_rn(eh, eh, f2(1.0f));
+    const float2 s = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+    const float2 q = __fmul2_rn(__fmul2_rn(__fmul2_rn(u, eh), s), eh);
+    return make_float2(__fsub_rn(fmaxf(x.x, 0.0f), q.x), __fsub_rn(fmaxf(x.y, 0.0f), q.y));
+  }
+}
+
+template <int A, bool kPrecise>
+__device__ __forceinline__ float2 act2_f(float2 x) {
+  if constexpr (A == kActGelu) return gelu2_f<kPrecise>(x);
+  else return silu2_f<kPrecise>(x);
+}
+
 template <int A, bool kPrecise>
 __device__ __forceinline__ float act_f(float x) {
   if constexpr (A == kActGelu) return gelu_f<kPrecise>(x);
@@ -227,7 +278,11 @@ __global__ void __launch_bounds__(256) act_fwd_vec(const uint4 *x, uint4 *y, uin
         if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
         else c = codes_vec_16<T, A>(v[j]);
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) f[k] = act_f<A, kPrecise>(f[k]);
+        for (int k = 0; k < kVec; k += 2) {
+          const float2 r = act2_f<A, kPrecise>(make_float2(f[k], f[k + 1]));
+          f[k] = r.x;
+          f[k + 1] = r.y;
+        }
         st_stream(y + i, Vec<T>::pack(f));
         cw[i] = (CodeWord<T>)c;
       }
