@@ -32,11 +32,11 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+def _compile(src: str, objdir: str = OBJ, defines=()) -> str:
+    obj = os.path.join(objdir, src.replace(".cu", ".o"))
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
     if _stale(obj, deps):
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(obj.replace(".o", ".ptxas.log"), "w") as f:
             f.write(r.stdout + r.stderr)
@@ -58,6 +58,19 @@ def build(force: bool = False) -> str:
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
     return LIB
+
+
+def build_variant(name: str, defines) -> str:
+    """Tuning aid: build liblmbp_<name>.so with extra -D defines into
+    _variants/ (used by tools/sweep.py; the product library is LIB)."""
+    vdir = os.path.join(HERE, "_variants", name)
+    os.makedirs(vdir, exist_ok=True)
+    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, vdir, defines), SOURCES))
+    out = os.path.join(HERE, "_variants", f"liblmbp_{name}.so")
+    if _stale(out, objs):
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
+    return out
 
 
 if __name__ == "__main__":

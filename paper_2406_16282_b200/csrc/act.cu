@@ -261,12 +261,23 @@ __global__ void __launch_bounds__(256) act_fwd_vec(const uint4 *x, uint4 *y, uin
   constexpr int kVec = Traits<T>::kVec;
   CodeWord<T> *cw = reinterpret_cast<CodeWord<T> *>(codes);
   const int64_t tile = (int64_t)blockDim.x * U;
-  for (int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x; base < nvec; base += (int64_t)gridDim.x * tile) {
-    uint4 v[U];
+  const int64_t stride = (int64_t)gridDim.x * tile;
+  // Register double buffering: the next tile's loads are in flight while the
+  // current tile is computed, so every warp always has U x 16 B per lane
+  // outstanding (the activation math is long enough to expose DRAM latency).
+  int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x;
+  uint4 v[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < nvec) v[j] = ld_stream(x + i);
+  }
+  for (; base < nvec; base += stride) {
+    uint4 nv[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int64_t i = base + (int64_t)j * blockDim.x;
-      if (i < nvec) v[j] = ld_stream(x + i);
+      const int64_t i = base + stride + (int64_t)j * blockDim.x;
+      if (i < nvec) nv[j] = ld_stream(x + i);
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -287,6 +298,8 @@ __global__ void __launch_bounds__(256) act_fwd_vec(const uint4 *x, uint4 *y, uin
         cw[i] = (CodeWord<T>)c;
       }
     }
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = nv[j];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && nvec * kVec < n)
     act_fwd_tail<T, A, kPrecise>(reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y), codes, nvec * kVec, n);
@@ -320,15 +333,27 @@ __global__ void __launch_bounds__(256) act_bwd_vec(const uint4 *dy, const uint8_
   constexpr int kVec = Traits<T>::kVec;
   const CodeWord<T> *cw = reinterpret_cast<const CodeWord<T> *>(codes);
   const int64_t tile = (int64_t)blockDim.x * U;
-  for (int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x; base < nvec; base += (int64_t)gridDim.x * tile) {
-    uint4 v[U];
-    uint32_t c[U];
+  const int64_t stride = (int64_t)gridDim.x * tile;
+  int64_t base = (int64_t)blockIdx.x * tile + threadIdx.x;
+  uint4 v[U];
+  uint32_t c[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < nvec) {
+      v[j] = ld_stream(dy + i);
+      c[j] = cw[i];
+    }
+  }
+  for (; base < nvec; base += stride) {
+    uint4 nv[U];
+    uint32_t nc[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int64_t i = base + (int64_t)j * blockDim.x;
+      const int64_t i = base + stride + (int64_t)j * blockDim.x;
       if (i < nvec) {
-        v[j] = ld_stream(dy + i);
-        c[j] = cw[i];
+        nv[j] = ld_stream(dy + i);
+        nc[j] = cw[i];
       }
     }
 #pragma unroll
@@ -341,6 +366,11 @@ __global__ void __launch_bounds__(256) act_bwd_vec(const uint4 *dy, const uint8_
         for (int k = 0; k < kVec; ++k) f[k] = __fmul_rn(f[k], level<A>((c[j] >> (2 * k)) & 3u));
         st_stream(dx + i, Vec<T>::pack(f));
       }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      v[j] = nv[j];
+      c[j] = nc[j];
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -358,6 +388,151 @@ __global__ void __launch_bounds__(256) act_bwd_scalar(const T *dy, const uint8_t
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t cj = (codes[j >> 2] >> (2 * (j & 3))) & 3u;
     dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), level<A>(cj)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined path (the default for 16-byte aligned tensors).
+//
+// One producer warp streams 16 KB tiles of the input (x, or dy + codes) into a
+// ring of kStages shared-memory stages with cp.async.bulk (the TMA engine, no
+// tensor map needed for contiguous data), completion on a per-stage mbarrier.
+// Eight consumer warps copy their part of a tile into registers, release the
+// stage at once (so the producer refills it while they compute), compute and
+// store straight to global with coalesced 16-byte stores.  Loads in flight
+// per SM = CTAs x stages x 16 KB, independent of the math latency -- this is
+// what the register-prefetch variant could not reach for GELU/SiLU.
+// ---------------------------------------------------------------------------
+// Pipeline shapes, tuned on B200 (tools/sweep.py; profiles/r01/sweep*.jsonl):
+// forward 16 consumer warps x 2 vectors/lane (16 KB tiles) x 4 stages;
+// backward 12 warps x 4 vectors/lane (24 KB tiles) x 3 stages.  Plain bulk
+// loads (no L2 evict-first hint: it cost 2-3 %).
+template <bool kFwd> struct TmaShape;
+template <> struct TmaShape<true> {
+  static constexpr int W = 16, U = 2, S = 4;
+};
+template <> struct TmaShape<false> {
+  static constexpr int W = 12, U = 4, S = 3;
+};
+template <bool kFwd> __host__ __device__ constexpr int tile_vec() {
+  return TmaShape<kFwd>::W * 32 * TmaShape<kFwd>::U;
+}
+template <bool kFwd> __host__ __device__ constexpr int tma_threads() { return (TmaShape<kFwd>::W + 1) * 32; }
+template <typename T, bool kFwd> __host__ __device__ constexpr int tile_code_bytes() {
+  return tile_vec<kFwd>() * Traits<T>::kVec / 4;
+}
+
+template <typename T, bool kFwd>
+constexpr size_t tma_smem_bytes() {
+  return (size_t)TmaShape<kFwd>::S * tile_vec<kFwd>() * 16 +
+         (kFwd ? 0 : (size_t)TmaShape<kFwd>::S * tile_code_bytes<T, kFwd>()) + 2 * TmaShape<kFwd>::S * sizeof(uint64_t);
+}
+
+template <typename T, int A, bool kPrecise, bool kFwd>
+__device__ __forceinline__ void act_vec_op(const uint4 &v, uint32_t c_in, uint4 *out, CodeWord<T> *cw, int64_t i) {
+  constexpr int kVec = Traits<T>::kVec;
+  float f[kVec];
+  Vec<T>::unpack(v, f);
+  if constexpr (kFwd) {
+    uint32_t c;
+    if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
+    else c = codes_vec_16<T, A>(v);
+#pragma unroll
+    for (int k = 0; k < kVec; k += 2) {
+      const float2 r = act2_f<A, kPrecise>(make_float2(f[k], f[k + 1]));
+      f[k] = r.x;
+      f[k + 1] = r.y;
+    }
+    st_stream(out + i, Vec<T>::pack(f));
+    cw[i] = (CodeWord<T>)c;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) f[k] = __fmul_rn(f[k], level<A>((c_in >> (2 * k)) & 3u));
+    st_stream(out + i, Vec<T>::pack(f));
+  }
+}
+
+template <typename T, int A, bool kPrecise, bool kFwd>
+__global__ void __launch_bounds__(tma_threads<kFwd>()) act_tma(const uint4 *in, const uint8_t *codes_in, uint4 *out,
+                                                               uint8_t *codes_out, int64_t nvec, int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kVec = Traits<T>::kVec;
+  constexpr int kTmaWarps = TmaShape<kFwd>::W, kTmaU = TmaShape<kFwd>::U, kStages = TmaShape<kFwd>::S;
+  constexpr int kTileVec = tile_vec<kFwd>();
+  constexpr int kCB = tile_code_bytes<T, kFwd>();
+  uint4 *buf = reinterpret_cast<uint4 *>(smem);
+  uint8_t *cbuf = smem + (size_t)kStages * kTileVec * 16;
+  uint64_t *full = reinterpret_cast<uint64_t *>(cbuf + (kFwd ? 0 : (size_t)kStages * kCB));
+  uint64_t *empty = full + kStages;
+  CodeWord<T> *cw_out = reinterpret_cast<CodeWord<T> *>(codes_out);
+  const CodeWord<T> *cw_in = reinterpret_cast<const CodeWord<T> *>(codes_in);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = nvec / kTileVec;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kTmaWarps) {  // producer
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % kStages;
+        const uint32_t ph = (uint32_t)(k / kStages) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], kTileVec * 16 + (kFwd ? 0 : kCB));
+        bulk_g2s(buf + (size_t)s * kTileVec, in + t * kTileVec, kTileVec * 16, &full[s]);
+        if constexpr (!kFwd) bulk_g2s(cbuf + (size_t)s * kCB, codes_in + t * kCB, kCB, &full[s]);
+      }
+    }
+  } else {  // consumers
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      const int s = k % kStages;
+      const uint32_t ph = (uint32_t)(k / kStages) & 1u;
+      mbar_wait(&full[s], ph);
+      uint4 v[kTmaU];
+      uint32_t c[kTmaU];
+#pragma unroll
+      for (int j = 0; j < kTmaU; ++j) {
+        const int vi = j * (kTmaWarps * 32) + warp * 32 + lane;
+        v[j] = lds128(buf + (size_t)s * kTileVec + vi);
+        if constexpr (!kFwd) c[j] = reinterpret_cast<const CodeWord<T> *>(cbuf + (size_t)s * kCB)[vi];
+        else c[j] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // stage may be refilled while we compute
+#pragma unroll
+      for (int j = 0; j < kTmaU; ++j) {
+        const int64_t i = t * kTileVec + j * (kTmaWarps * 32) + warp * 32 + lane;
+        act_vec_op<T, A, kPrecise, kFwd>(v[j], c[j], out, cw_out, i);
+      }
+    }
+    // leftover vectors (< one tile) and the ragged scalar tail: CTA 0
+    if (blockIdx.x == 0) {
+      for (int64_t i = ntiles * kTileVec + threadIdx.x; i < nvec; i += kTmaWarps * 32) {
+        const uint4 v = ld_stream(in + i);
+        act_vec_op<T, A, kPrecise, kFwd>(v, kFwd ? 0u : (uint32_t)cw_in[i], out, cw_out, i);
+      }
+      if (threadIdx.x == 0 && nvec * kVec < n) {
+        if constexpr (kFwd) {
+          act_fwd_tail<T, A, kPrecise>(reinterpret_cast<const T *>(in), reinterpret_cast<T *>(out), codes_out,
+                                       nvec * kVec, n);
+        } else {
+          const T *dys = reinterpret_cast<const T *>(in);
+          T *dxs = reinterpret_cast<T *>(out);
+          for (int64_t j = nvec * kVec; j < n; ++j) {
+            const uint32_t cj = (codes_in[j >> 2] >> (2 * (j & 3))) & 3u;
+            dxs[j] = from_f32<T>(__fmul_rn(to_f32<T>(dys[j]), level<A>(cj)));
+          }
+        }
+      }
+    }
   }
 }
 
@@ -383,7 +558,22 @@ static cudaError_t act_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, 
   const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                        (kVec == 4 || (uintptr_t)codes % 2 == 0);
   const int sms = sm_count();
-  if (aligned) {
+  if (aligned && n >= (int64_t)tile_vec<true>() * kVec) {
+    auto kern = act_tma<T, A, kPrecise, true>;
+    constexpr size_t smem = tma_smem_bytes<T, true>();
+    constexpr int threads = tma_threads<true>();
+    static const int occ = [&] {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem) != cudaSuccess || b < 1) b = 1;
+      return b;
+    }();
+    const int64_t nvec = n / kVec;
+    const int64_t want = std::max<int64_t>(1, nvec / tile_vec<true>());
+    const int grid = (int)std::min<int64_t>(want, (int64_t)sms * occ);
+    kern<<<grid, threads, smem, s>>>(reinterpret_cast<const uint4 *>(x), nullptr, reinterpret_cast<uint4 *>(y),
+                                         codes, nvec, n);
+  } else if (aligned) {
     auto kern = act_fwd_vec<T, A, kPrecise, kActUnroll>;
     static const int occ = occupancy(kern, kActThreads);
     const int64_t nvec = n / kVec;
@@ -407,7 +597,22 @@ static cudaError_t act_bwd_t(const void *dy, const uint8_t *codes, void *dx, int
   const bool aligned = ((uintptr_t)dy % 16 == 0) && ((uintptr_t)dx % 16 == 0) &&
                        (kVec == 4 || (uintptr_t)codes % 2 == 0);
   const int sms = sm_count();
-  if (aligned) {
+  if (aligned && (uintptr_t)codes % 16 == 0 && n >= (int64_t)tile_vec<false>() * kVec) {
+    auto kern = act_tma<T, A, false, false>;
+    constexpr size_t smem = tma_smem_bytes<T, false>();
+    constexpr int threads = tma_threads<false>();
+    static const int occ = [&] {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem) != cudaSuccess || b < 1) b = 1;
+      return b;
+    }();
+    const int64_t nvec = n / kVec;
+    const int64_t want = std::max<int64_t>(1, nvec / tile_vec<false>());
+    const int grid = (int)std::min<int64_t>(want, (int64_t)sms * occ);
+    kern<<<grid, threads, smem, s>>>(reinterpret_cast<const uint4 *>(dy), codes, reinterpret_cast<uint4 *>(dx),
+                                         nullptr, nvec, n);
+  } else if (aligned) {
     auto kern = act_bwd_vec<T, A, kActUnroll>;
     static const int occ = occupancy(kern, kActThreads);
     const int64_t nvec = n / kVec;

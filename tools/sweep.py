@@ -1,0 +1,102 @@
+"""Tuning sweep: time one kernel of several liblmbp variants (built with
+different -D parameters by paper_2406_16282_b200.build.build_variant) on a
+BASELINE config shape, L2 flushed (read of 2 x L2) before every launch, CUDA
+events on the launching stream.  Prints one JSON line per (variant, kernel).
+
+    python tools/sweep.py --config c4 --variants base:  s3:LMBP_TMA_STAGES=3 ...
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2406_16282_b200 import build as B  # noqa: E402
+from paper_2406_16282_b200._lib import SIGNATURES  # noqa: E402
+
+DT = {"f32": 0, "bf16": 1, "f16": 2}
+
+
+def load(path):
+    L = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--variants", nargs="+", default=["base:"])
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--kernels", default="act_fwd,act_bwd,norm_fwd,norm_bwd")
+    ap.add_argument("--build-only", action="store_true")
+    a = ap.parse_args()
+    libs = {}
+    for v in a.variants:
+        name, _, defs = v.partition(":")
+        libs[name] = B.build_variant(name, [d for d in defs.split(",") if d])
+    if a.build_only:
+        return
+    cfg = synth.CONFIGS[a.config]
+    R, F, H, dt = cfg["R"], cfg["F"], cfg["H"], cfg["dtype"]
+    dev = torch.device("cuda")
+    x = synth.act_input(R, F, dt, device=dev)
+    dy = synth.grad_input(R, F, dt, device=dev)
+    y, dx = torch.empty_like(x), torch.empty_like(dy)
+    codes = torch.empty((R * F + 3) // 4, dtype=torch.uint8, device=dev)
+    xn = synth.norm_input(R, H, dt, device=dev)
+    gn = synth.grad_input(R, H, dt, device=dev)
+    yn, dxn = torch.empty_like(xn), torch.empty_like(gn)
+    rstd = torch.empty(R, dtype=torch.float32, device=dev)
+    flush = torch.ones((2 * torch.cuda.get_device_properties(dev).L2_cache_size) // 4, device=dev)
+    sink = torch.zeros((), device=dev)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+    b = synth.ELEM_BYTES[dt]
+    n = R * F
+    nbytes = {"act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
+              "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R}
+    act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
+    nrm = "msln" if cfg["norm"] == "ln" else "msrms"
+    for name, path in libs.items():
+        L = load(path)
+        calls = {
+            "act_fwd": lambda: getattr(L, act + "_fwd")(x.data_ptr(), y.data_ptr(), codes.data_ptr(), R, F, DT[dt], sp),
+            "act_bwd": lambda: getattr(L, act + "_bwd")(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), R, F, DT[dt], sp),
+            "norm_fwd": lambda: getattr(L, nrm + "_fwd")(xn.data_ptr(), yn.data_ptr(), rstd.data_ptr(), R, H, 1e-6,
+                                                         DT[dt], sp),
+            "norm_bwd": lambda: getattr(L, nrm + "_bwd")(gn.data_ptr(), yn.data_ptr(), rstd.data_ptr(), dxn.data_ptr(),
+                                                         R, H, DT[dt], sp),
+        }
+        calls["act_fwd"]()
+        calls["norm_fwd"]()
+        for k in a.kernels.split(","):
+            for _ in range(3):
+                calls[k]()
+            ts = []
+            for _ in range(a.iters):
+                sink.copy_(flush.sum())
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                rc = calls[k]()
+                e1.record(st)
+                assert rc == 0, rc
+                ts.append((e0, e1))
+            torch.cuda.synchronize()
+            us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ts)
+            med = us[len(us) // 2]
+            print(json.dumps({"variant": name, "config": a.config, "kernel": k, "us_med": round(med, 2),
+                              "us_min": round(us[0], 2), "GB/s": round(nbytes[k] / med / 1e3, 1),
+                              "frac": round(nbytes[k] / med / 1e3 / 6536, 4)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
