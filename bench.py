@@ -53,6 +53,7 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the full config (its own batch); "
@@ -362,14 +363,14 @@ def main():
         h2d = sum(t.numel() * t.element_size() for t in (hx, hdy, hxn, hgn))
         d2h = sum(t.numel() * t.element_size() for t in houts)
 
-        # Rows are processed in chunks round-robin over two streams, so the
+        # Rows are processed in chunks round-robin over several streams, so the
         # H2D copy of chunk c+1, the kernels of chunk c and the D2H copy of
         # chunk c-1 overlap (PCIe is full duplex).  Codes of a row block are a
         # contiguous byte range because F % 4 == 0 in every config.
         assert F % 4 == 0
         nchunk = max(1, min(args.e2e_chunks, R))
         bounds = [(R * c) // nchunk for c in range(nchunk + 1)]
-        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        streams = [torch.cuda.Stream(dev) for _ in range(args.e2e_streams)]
         hy, hcodes, hdx, hyn, hrstd, hdxn = houts
 
         def e2e_chunk(r0, r1, s):
@@ -396,7 +397,7 @@ def main():
             for s_ in streams:
                 s_.wait_event(start)
             for c in range(nchunk):
-                e2e_chunk(bounds[c], bounds[c + 1], streams[c % 2])
+                e2e_chunk(bounds[c], bounds[c + 1], streams[c % len(streams)])
             for s_ in streams:
                 done = torch.cuda.Event()
                 done.record(s_)
@@ -419,7 +420,7 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(te.item() / args.e2e_steps, 3),
                "path": f"pinned host -> H2D -> C-ABI kernels -> D2H pinned host; {nchunk} row chunks "
-                       "round-robin on 2 streams (copies overlap kernels and each other)"}
+                       f"round-robin on {len(streams)} streams (copies overlap kernels and each other)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

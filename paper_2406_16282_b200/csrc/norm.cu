@@ -202,6 +202,171 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
 }
 
 // ---------------------------------------------------------------------------
+// TMA-pipelined path (default for aligned rows that fit the shared-memory
+// ring).  Every warp owns rows gw, gw + GW, ... (GW = warps in the grid) and
+// streams them through its own ring of S stages: lane 0 issues cp.async.bulk
+// copies of the next S rows (x; or dy and y) completing on the stage's
+// mbarrier; the warp reduces and writes the current row from shared memory.
+// No CTA-level synchronisation at all: reductions are warp butterflies over
+// lane partials accumulated in a fixed order -> deterministic.
+// ---------------------------------------------------------------------------
+template <typename T, int NORM, bool kFwd>
+__device__ __forceinline__ void norm_issue(uint8_t *stage, uint64_t *bar, const uint4 *a, const uint4 *b, int64_t row,
+                                           int nvec) {
+  const uint32_t rowbytes = (uint32_t)nvec * 16u;
+  mbar_arrive_expect_tx(bar, kFwd ? rowbytes : 2u * rowbytes);
+  bulk_g2s(stage, a + row * nvec, rowbytes, bar);
+  if constexpr (!kFwd) bulk_g2s(stage + rowbytes, b + row * nvec, rowbytes, bar);
+}
+
+template <typename T, int NORM, bool kFwd>
+__global__ void __launch_bounds__(512) norm_tma(const uint4 *a, const uint4 *b, const float *rstd_in, uint4 *out,
+                                                float *rstd_out, int64_t rows, int nvec, int cols, float eps,
+                                                int stages) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kVec = Traits<T>::kVec;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  const int stage_bytes = nvec * 16 * (kFwd ? 1 : 2);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem) + warp * stages;
+  uint8_t *ring = smem + ((W * stages * 8 + 127) & ~127) + (size_t)warp * stages * stage_bytes;
+  const int64_t gw = (int64_t)blockIdx.x * W + warp, GW = (int64_t)gridDim.x * W;
+  const float fcols = (float)cols;
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+    for (int s = 0; s < stages; ++s) {
+      const int64_t row = gw + s * GW;
+      if (row < rows) norm_issue<T, NORM, kFwd>(ring + (size_t)s * stage_bytes, &full[s], a, b, row, nvec);
+    }
+  }
+  __syncwarp();
+  int k = 0;
+  for (int64_t row = gw; row < rows; row += GW, ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)(k / stages) & 1u);
+    const uint4 *sa = reinterpret_cast<const uint4 *>(ring + (size_t)s * stage_bytes);
+    uint4 *orow = out + row * nvec;
+    if constexpr (kFwd) {
+      float mean = 0.0f;
+      if constexpr (NORM == kNormLN) {
+        float s0 = 0.0f, s1 = 0.0f;
+        for (int vi = lane; vi < nvec; vi += 32) {
+          float f[kVec];
+          Vec<T>::unpack(lds128(sa + vi), f);
+#pragma unroll
+          for (int e = 0; e < kVec; e += 2) {
+            s0 += f[e];
+            s1 += f[e + 1];
+          }
+        }
+        mean = __fdiv_rn(warp_sum(s0 + s1), fcols);
+      }
+      float q0 = 0.0f, q1 = 0.0f;
+      for (int vi = lane; vi < nvec; vi += 32) {
+        float f[kVec];
+        Vec<T>::unpack(lds128(sa + vi), f);
+#pragma unroll
+        for (int e = 0; e < kVec; e += 2) {
+          const float d0 = __fsub_rn(f[e], mean), d1 = __fsub_rn(f[e + 1], mean);
+          q0 = fmaf(d0, d0, q0);
+          q1 = fmaf(d1, d1, q1);
+        }
+      }
+      const float r = rsqrtf(__fadd_rn(__fdiv_rn(warp_sum(q0 + q1), fcols), eps));
+      for (int vi = lane; vi < nvec; vi += 32) {
+        float f[kVec];
+        Vec<T>::unpack(lds128(sa + vi), f);
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) f[e] = __fmul_rn(__fsub_rn(f[e], mean), r);
+        st_stream(orow + vi, Vec<T>::pack(f));
+      }
+      if (lane == 0) rstd_out[row] = r;
+    } else {
+      const uint4 *sb = sa + nvec;
+      const float r = rstd_in[row];
+      float g0 = 0.0f, g1 = 0.0f, p0 = 0.0f, p1 = 0.0f;
+      for (int vi = lane; vi < nvec; vi += 32) {
+        float g[kVec], h[kVec];
+        Vec<T>::unpack(lds128(sa + vi), g);
+        Vec<T>::unpack(lds128(sb + vi), h);
+#pragma unroll
+        for (int e = 0; e < kVec; e += 2) {
+          if constexpr (NORM == kNormLN) {
+            g0 += g[e];
+            g1 += g[e + 1];
+          }
+          p0 = fmaf(g[e], h[e], p0);
+          p1 = fmaf(g[e + 1], h[e + 1], p1);
+        }
+      }
+      const float2 acc = warp_sum2(make_float2(g0 + g1, p0 + p1));
+      const float m1 = NORM == kNormLN ? __fdiv_rn(acc.x, fcols) : 0.0f;
+      const float m2 = __fdiv_rn(acc.y, fcols);
+      for (int vi = lane; vi < nvec; vi += 32) {
+        float g[kVec], h[kVec];
+        Vec<T>::unpack(lds128(sa + vi), g);
+        Vec<T>::unpack(lds128(sb + vi), h);
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const float c = NORM == kNormLN ? __fsub_rn(g[e], m1) : g[e];
+          g[e] = __fmul_rn(r, fmaf(-h[e], m2, c));
+        }
+        st_stream(orow + vi, Vec<T>::pack(g));
+      }
+    }
+    __syncwarp();  // every lane has finished reading stage s
+    if (lane == 0) {
+      const int64_t nr = row + (int64_t)stages * GW;
+      if (nr < rows) norm_issue<T, NORM, kFwd>(ring + (size_t)s * stage_bytes, &full[s], a, b, nr, nvec);
+    }
+  }
+}
+
+struct TmaPlan {
+  bool ok;
+  int warps, stages;
+  size_t smem;
+};
+
+// Shared-memory budget per CTA for the ring (B200: 227 KB opt-in per CTA).
+constexpr size_t kNormSmemBudget = 200 * 1024;
+
+static TmaPlan plan_tma(int nvec, bool fwd) {
+  const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
+  TmaPlan p{false, 0, 0, 0};
+  int stages = stage <= 4096 ? 4 : (stage <= 12288 ? 3 : 2);
+  int warps = (int)std::min<size_t>(16, kNormSmemBudget / (stages * stage));
+  while (warps < 1 && stages > 2) {
+    --stages;
+    warps = (int)std::min<size_t>(16, kNormSmemBudget / (stages * stage));
+  }
+  if (warps < 1) return p;
+  p.ok = true;
+  p.warps = warps;
+  p.stages = stages;
+  p.smem = ((size_t)warps * stages * 8 + 127) / 128 * 128 + (size_t)warps * stages * stage;
+  return p;
+}
+
+template <typename T, int NORM, bool kFwd>
+static void launch_norm_tma(const TmaPlan &tp, const void *a, const void *b, const float *rstd_in, void *out,
+                            float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps, cudaStream_t s) {
+  auto kern = norm_tma<T, NORM, kFwd>;
+  static int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = 1;
+  }
+  const int threads = tp.warps * 32;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, tp.smem) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t want = (rows + tp.warps - 1) / tp.warps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
+  kern<<<grid, threads, tp.smem, s>>>(reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), rstd_in,
+                                      reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec, (int)cols, eps, tp.stages);
+}
+
+// ---------------------------------------------------------------------------
 // Scalar multi-pass fallback (any alignment / any length): one CTA per row.
 // ---------------------------------------------------------------------------
 template <typename T, int NORM>
@@ -344,6 +509,18 @@ template <typename T, int NORM>
 static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
                               cudaStream_t s) {
   const RowPlan p = plan_rows<T>(cols, x, y, y);
+  // Forward: the register-resident team kernel measured faster than the TMA
+  // ring at every BASELINE shape (C4 21.9 vs 23.5 us, C5 104 vs 117 us), so
+  // the ring is only used where registers cannot hold a row.
+  if (!p.vec) {
+    const int64_t nv = cols / Traits<T>::kVec;
+    const bool ok16 = cols % Traits<T>::kVec == 0 && (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
+    const TmaPlan tp = ok16 && nv < (1 << 26) ? plan_tma((int)nv, true) : TmaPlan{false, 0, 0, 0};
+    if (tp.ok) {
+      launch_norm_tma<T, NORM, true>(tp, x, nullptr, nullptr, y, rstd, rows, (int)nv, cols, eps, s);
+      return cudaGetLastError();
+    }
+  }
   if (!p.vec) {
     auto k = norm_fwd_scalar<T, NORM>;
     launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
@@ -373,6 +550,21 @@ template <typename T, int NORM>
 static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
                               int64_t cols, cudaStream_t s) {
   const RowPlan p = plan_rows<T>(cols, dy, y, dx);
+  // Backward: the TMA ring wins once a row pair (dy, y) is >= 8 KB (C4: 32.8
+  // vs 34.6 us, C5: 160 vs 172 us); short rows (H = 768) stay on the register
+  // team kernel (C2/C3 measured faster there).  Rows too long for registers
+  // also take the ring when it fits.
+  {
+    const int64_t nv = cols / Traits<T>::kVec;
+    const bool ok16 = cols % Traits<T>::kVec == 0 && (uintptr_t)dy % 16 == 0 && (uintptr_t)y % 16 == 0 &&
+                      (uintptr_t)dx % 16 == 0;
+    const bool want = ok16 && (!p.vec || nv * 32 >= 8192) && nv < (1 << 26);
+    const TmaPlan tp = want ? plan_tma((int)nv, false) : TmaPlan{false, 0, 0, 0};
+    if (tp.ok) {
+      launch_norm_tma<T, NORM, false>(tp, dy, y, rstd, dx, nullptr, rows, (int)nv, cols, 0.0f, s);
+      return cudaGetLastError();
+    }
+  }
   if (!p.vec) {
     auto k = norm_bwd_scalar<T, NORM>;
     launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(dy),
