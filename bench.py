@@ -239,6 +239,59 @@ def run_reference(args):
     return 0
 
 
+def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
+    """the fused ReSwiGLU2 gate (h = SiLU(gate) * up with
+    ReSiLU2's backward) against the unfused composition (resilu2 kernels +
+    torch elementwise mul) on the same [R, F] tensors, L2 flushed before every
+    launch.  Reported beside the headline; not part of its step."""
+    b = gate.element_size()
+    n = gate.numel()
+    h, a = torch.empty_like(gate), torch.empty_like(gate)
+    codes = torch.empty(P.codes_bytes(n), dtype=torch.uint8, device=gate.device)
+    dh = up  # any [R, F] tensor in HBM
+    dg, du = torch.empty_like(gate), torch.empty_like(gate)
+    a2 = torch.empty_like(gate)
+    fused = {
+        "fwd": lambda: P.reswiglu2_fwd(gate, up, h=h, a=a, codes=codes, stream=stream),
+        "bwd": lambda: P.reswiglu2_bwd(dh, up, a, codes, dgate=dg, dup=du, stream=stream),
+    }
+
+    def unfused_fwd():
+        P.resilu2_fwd(gate, y=a2, codes=codes, stream=stream)
+        torch.mul(a2, up, out=h)
+
+    def unfused_bwd():
+        torch.mul(dh, a2, out=du)
+        torch.mul(dh, up, out=dg)
+        P.resilu2_bwd(dg, codes, dx=dg, stream=stream)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        evs = []
+        for _ in range(iters):
+            sink.copy_(flush.sum())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(e0.elapsed_time(e1) for e0, e1 in evs) / iters * 1e3
+
+    bf, bb = (4 * b * n + (n + 3) // 4), (5 * b * n + (n + 3) // 4)
+    tf, tb = timeit(fused["fwd"]), timeit(fused["bwd"])
+    uf, ub = timeit(unfused_fwd), timeit(unfused_bwd)
+    return {"shape": list(gate.shape), "fused_fwd_us": round(tf, 2), "fused_bwd_us": round(tb, 2),
+            "fused_GB/s": round((bf + bb) / (tf + tb) / 1e3, 1),
+            "fused_frac": round((bf + bb) / (tf + tb) / 1e3 / 6536.0, 4),
+            "unfused_fwd_us": round(uf, 2), "unfused_bwd_us": round(ub, 2),
+            "speedup_fwd_bwd": round((uf + ub) / (tf + tb), 3),
+            "algorithmic_bytes": {"fwd": bf, "bwd": bb},
+            "saved_bytes_per_layer": {"exact_silu_mul": 3 * b * n, "reswiglu2": 2 * b * n + (n + 3) // 4},
+            "gpu_launches": 2 * iters}
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -422,6 +475,8 @@ def main():
                "path": f"pinned host -> H2D -> C-ABI kernels -> D2H pinned host; {nchunk} row chunks "
                        f"round-robin on {len(streams)} streams (copies overlap kernels and each other)"}
 
+    swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.eps, args.cpu_seconds)
@@ -444,6 +499,7 @@ def main():
                                     / (max_ms / 1e3), 1),
             "per_rank_ms": [round(m, 3) for m in ms_all],
             "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
+            "reswiglu2": swiglu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -151,6 +151,32 @@ LMBP_API int msrms_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_
 LMBP_API int msrms_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
               int64_t cols, int dtype, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * ReSwiGLU2: fused LLaMA gate h = SiLU(gate) * up with ReSiLU2's backward
+ * (SwiGLU; ReSiLU2).  Semantics are
+ * exactly those of the unfused composition resilu2_fwd -> elementwise mul
+ * (and its reverse), with one HBM pass instead of three:
+ * Forward:  a = RN_dtype(SiLU(gate))        -- saved (the mul's operand)
+ *           h = RN_dtype(RN32(a * up))       -- output
+ *           codes of gate as resilu2_fwd     -- saved (2 bits / element)
+ *           gate, up: [rows, cols]; h, a: [rows, cols] outputs;
+ *           codes: lmbp_codes_bytes(rows*cols) bytes.
+ *           Activation memory kept for backward: a, up and codes (2b + 1/4
+ *           bytes per element) instead of gate, up and SiLU(gate) (3b).
+ * Backward: dup   = RN_dtype(RN32(dh * a))
+ *           dgate = RN_dtype(RN32(RN_dtype(RN32(dh * up)) * RN32(s[code])))
+ *           dh, up, a: [rows, cols]; codes as written by reswiglu2_fwd;
+ *           dgate, dup: [rows, cols] outputs.
+ * Vector path: all tensor pointers 16-byte aligned (forward: codes 2-byte
+ * aligned for 16-bit dtypes; backward: codes 16-byte aligned), else a scalar
+ * path with bitwise-identical results.  Any output may exactly alias any
+ * input of the same shape.  Errors as above.
+ * ------------------------------------------------------------------------- */
+LMBP_API int reswiglu2_fwd(const void *gate, const void *up, void *h, void *a, uint8_t *codes, int64_t rows,
+                           int64_t cols, int dtype, void *stream);
+LMBP_API int reswiglu2_bwd(const void *dh, const void *up, const void *a, const uint8_t *codes, void *dgate,
+                           void *dup, int64_t rows, int64_t cols, int dtype, void *stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -77,6 +77,10 @@ def lib():
             f = getattr(L, name)
             f.restype, f.argtypes = i32, [p, p, p, i64, i64, p, i32]
         L.oracle_max_threads.restype, L.oracle_max_threads.argtypes = i32, []
+        L.oracle_reswiglu2_fwd.restype = i32
+        L.oracle_reswiglu2_fwd.argtypes = [p, p, i64, p, p, p, i32]
+        L.oracle_reswiglu2_bwd.restype = i32
+        L.oracle_reswiglu2_bwd.argtypes = [p, p, p, p, i64, p, p, i32]
         _lib = L
     return _lib
 
@@ -285,6 +289,52 @@ def msrms_bwd(dy64, y64, rstd64, nthreads=None):
     if R:
         assert lib().oracle_msrms_bwd(_ptr(dy), _ptr(y), _ptr(rstd), R, H, _ptr(dx), _nt(nthreads)) == 0
     return dx
+
+
+# --------------------------------------------------------------------------
+# ReSwiGLU2: h = SiLU(gate) * up, ReSiLU2 backward
+# --------------------------------------------------------------------------
+def reswiglu2_fwd(g64, u64, nthreads=None):
+    """(h = SiLU(g) u, a = SiLU(g), codes of g) in float64."""
+    g = np.ascontiguousarray(g64, dtype=np.float64).reshape(-1)
+    u = np.ascontiguousarray(u64, dtype=np.float64).reshape(-1)
+    if g.size != u.size:
+        raise ValueError("shape mismatch")
+    n = g.size
+    h, a = np.empty(n), np.empty(n)
+    codes = np.zeros(codes_bytes(n), dtype=np.uint8)
+    if n:
+        assert lib().oracle_reswiglu2_fwd(_ptr(g), _ptr(u), n, _ptr(h), _ptr(a), _ptr(codes), _nt(nthreads)) == 0
+    shp = np.shape(g64)
+    return h.reshape(shp), a.reshape(shp), codes
+
+
+def reswiglu2_bwd(dh64, u64, a64, codes, nthreads=None):
+    """Value mode: (dg = dh u s[code], du = dh a) in float64."""
+    dh = np.ascontiguousarray(dh64, dtype=np.float64).reshape(-1)
+    u = np.ascontiguousarray(u64, dtype=np.float64).reshape(-1)
+    a = np.ascontiguousarray(a64, dtype=np.float64).reshape(-1)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = dh.size
+    if u.size != n or a.size != n or codes.size != codes_bytes(n):
+        raise ValueError("shape mismatch")
+    dg, du = np.empty(n), np.empty(n)
+    if n:
+        assert lib().oracle_reswiglu2_bwd(_ptr(dh), _ptr(u), _ptr(a), _ptr(codes), n, _ptr(dg), _ptr(du),
+                                          _nt(nthreads)) == 0
+    shp = np.shape(dh64)
+    return dg.reshape(shp), du.reshape(shp)
+
+
+def reswiglu2_bwd_contract(dh_st, u_st, a_st, codes, dtype):
+    """Bitwise contract of the fused kernel = the unfused composition:
+    du = RN_T(RN32(dh a)); da = RN_T(RN32(dh u)); dg = act_bwd_contract(da).
+    Products of two binary32 values are exact in binary64."""
+    dh, u, a = decode(dh_st, dtype), decode(u_st, dtype), decode(a_st, dtype)
+    du = round_to(dh * a, dtype)
+    da = round_to(dh * u, dtype)
+    dg = act_bwd_contract("silu", codes, da, dtype)
+    return dg, du
 
 
 # --------------------------------------------------------------------------

@@ -287,6 +287,38 @@ int oracle_msrms_bwd(const double *dy, const double *y, const double *rstd, int6
     return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* ReSwiGLU2: LLaMA's SwiGLU gate            */
+/*   h = SiLU(g) * u  with SiLU replaced by ReSiLU2:           */
+/* forward exact, backward through the step derivative:                      */
+/*   a = SiLU(g), h = a u, code = #{i : g > c_i}  (SiLU table)       */
+/*   du = dh a,   dg = dh u s[code]                                           */
+/* ------------------------------------------------------------------------ */
+int oracle_reswiglu2_fwd(const double *g, const double *u, int64_t n, double *h, double *a, uint8_t *codes,
+                         int nthreads)
+{
+    int rc = oracle_act_fwd(ORACLE_SILU, g, n, a, codes, nthreads);
+    if (rc != 0) return rc;
+    (void)nthreads;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t j = 0; j < n; ++j) h[j] = a[j] * u[j];
+    return 0;
+}
+
+int oracle_reswiglu2_bwd(const double *dh, const double *u, const double *a, const uint8_t *codes, int64_t n,
+                         double *dg, double *du, int nthreads)
+{
+    double c[3], s[4], w[2];
+    if (oracle_step_table(ORACLE_SILU, c, s, w) != 0) return -1;
+    (void)nthreads;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t j = 0; j < n; ++j) {
+        du[j] = dh[j] * a[j];
+        dg[j] = dh[j] * u[j] * s[code_at(codes, j)];
+    }
+    return 0;
+}
+
 /* Number of OpenMP threads a parallel region would use (for reporting). */
 int oracle_max_threads(void)
 {

@@ -27,6 +27,8 @@ SIGNATURES = {
     "msln_bwd": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "msrms_fwd": (_i32, [_p, _p, _p, _i64, _i64, _f32, _i32, _p]),
     "msrms_bwd": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "reswiglu2_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "reswiglu2_bwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
 }
 
 LMBP_OK, LMBP_ERR_NULLPTR, LMBP_ERR_SHAPE, LMBP_ERR_DTYPE, LMBP_ERR_EPS, LMBP_ERR_CUDA, LMBP_ERR_KIND = range(7)

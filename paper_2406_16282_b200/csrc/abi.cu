@@ -70,6 +70,26 @@ static int norm_bwd_entry(int kind, const void *dy, const void *y, const float *
   return status_of(norm_bwd(kind, dtype, dy, y, rstd, dx, rows, cols, static_cast<cudaStream_t>(stream)));
 }
 
+static int swiglu_fwd_entry(const void *g, const void *u, void *h, void *a, uint8_t *codes, int64_t rows,
+                            int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!g || !u || !h || !a || !codes) return LMBP_ERR_NULLPTR;
+  return status_of(swiglu_fwd(dtype, g, u, h, a, codes, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
+static int swiglu_bwd_entry(const void *dh, const void *u, const void *a, const uint8_t *codes, void *dg, void *du,
+                            int64_t rows, int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!dh || !u || !a || !codes || !dg || !du) return LMBP_ERR_NULLPTR;
+  return status_of(swiglu_bwd(dtype, dh, u, a, codes, dg, du, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
 }  // namespace lmbp
 
 extern "C" {
@@ -133,6 +153,15 @@ int msrms_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, f
 int msrms_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows, int64_t cols, int dtype,
               void *stream) {
   return lmbp::norm_bwd_entry(lmbp::kNormRMS, dy, y, rstd, dx, rows, cols, dtype, stream);
+}
+
+int reswiglu2_fwd(const void *gate, const void *up, void *h, void *a, uint8_t *codes, int64_t rows, int64_t cols,
+                  int dtype, void *stream) {
+  return lmbp::swiglu_fwd_entry(gate, up, h, a, codes, rows, cols, dtype, stream);
+}
+int reswiglu2_bwd(const void *dh, const void *up, const void *a, const uint8_t *codes, void *dgate, void *dup,
+                  int64_t rows, int64_t cols, int dtype, void *stream) {
+  return lmbp::swiglu_bwd_entry(dh, up, a, codes, dgate, dup, rows, cols, dtype, stream);
 }
 
 }  // extern "C"

@@ -18,4 +18,9 @@ cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, i
 cudaError_t norm_bwd(int kind, int dtype, const void *dy, const void *y, const float *rstd, void *dx,
                      int64_t rows, int64_t cols, cudaStream_t s);
 
+cudaError_t swiglu_fwd(int dtype, const void *g, const void *u, void *h, void *a, uint8_t *codes, int64_t n,
+                       cudaStream_t s);
+cudaError_t swiglu_bwd(int dtype, const void *dh, const void *u, const void *a, const uint8_t *codes, void *dg,
+                       void *du, int64_t n, cudaStream_t s);
+
 }  // namespace lmbp

@@ -154,3 +154,47 @@ def step_table(kind: str):
     check("lmbp_step_table", lib().lmbp_step_table({"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}[kind],
                                                    ctypes.addressof(t), ctypes.addressof(lv)))
     return list(t), list(lv)
+
+
+def reswiglu2_fwd(gate, up, h=None, a=None, codes=None, stream=None):
+    """Fused ReSwiGLU2 forward: (h = RN(a * up), a = RN(SiLU(gate)), codes of
+    gate).  lmbp.h reswiglu2_fwd."""
+    _need(gate, "gate")
+    _need(up, "up")
+    n = gate.numel()
+    h = torch.empty_like(gate) if h is None else _need(h, "h")
+    a = torch.empty_like(gate) if a is None else _need(a, "a")
+    codes = (torch.empty(codes_bytes(n), dtype=torch.uint8, device=gate.device) if codes is None
+             else _need(codes, "codes"))
+    for t in (up, h, a):
+        if t.shape != gate.shape or t.dtype != gate.dtype:
+            raise ValueError("reswiglu2_fwd: shape/dtype mismatch")
+    if codes.numel() != codes_bytes(n):
+        raise ValueError("reswiglu2_fwd: codes size")
+    rows, cols = _rc(gate)
+    if n == 0:
+        return h, a, codes
+    check("reswiglu2_fwd", lib().reswiglu2_fwd(gate.data_ptr(), up.data_ptr(), h.data_ptr(), a.data_ptr(),
+                                               codes.data_ptr(), rows, cols, _dtype(gate), _stream(stream)))
+    return h, a, codes
+
+
+def reswiglu2_bwd(dh, up, a, codes, dgate=None, dup=None, stream=None):
+    """Fused ReSwiGLU2 backward: (dgate, dup).  lmbp.h reswiglu2_bwd."""
+    for t, nm in ((dh, "dh"), (up, "up"), (a, "a"), (codes, "codes")):
+        _need(t, nm)
+    n = dh.numel()
+    dgate = torch.empty_like(dh) if dgate is None else _need(dgate, "dgate")
+    dup = torch.empty_like(dh) if dup is None else _need(dup, "dup")
+    for t in (up, a, dgate, dup):
+        if t.shape != dh.shape or t.dtype != dh.dtype:
+            raise ValueError("reswiglu2_bwd: shape/dtype mismatch")
+    if codes.numel() != codes_bytes(n) or codes.dtype != torch.uint8:
+        raise ValueError("reswiglu2_bwd: codes size")
+    rows, cols = _rc(dh)
+    if n == 0:
+        return dgate, dup
+    check("reswiglu2_bwd", lib().reswiglu2_bwd(dh.data_ptr(), up.data_ptr(), a.data_ptr(), codes.data_ptr(),
+                                               dgate.data_ptr(), dup.data_ptr(), rows, cols, _dtype(dh),
+                                               _stream(stream)))
+    return dgate, dup

@@ -25,7 +25,7 @@ def declared_symbols():
 
 def test_header_declares_the_north_star_entry_points():
     names = set(declared_symbols())
-    for n in ("regelu2_fwd", "regelu2_bwd", "resilu2_fwd", "resilu2_bwd", "msln_fwd", "msln_bwd", "msrms_fwd",
+    for n in ("regelu2_fwd", "regelu2_bwd", "resilu2_fwd", "resilu2_bwd", "msln_fwd", "msln_bwd", "msrms_fwd", "reswiglu2_fwd", "reswiglu2_bwd",
               "msrms_bwd", "lmbp_codes_bytes", "lmbp_status_string", "lmbp_step_table", "lmbp_version"):
         assert n in names
 
@@ -93,6 +93,12 @@ def test_validation_without_device_work():
         assert fn(fake, fake, None, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
         assert fn(fake, fake, fake, fake, -2, 4, 0, None) == S.LMBP_ERR_SHAPE
         assert fn(fake, fake, fake, fake, 2, 4, 9, None) == S.LMBP_ERR_DTYPE
+    assert L.reswiglu2_fwd(fake, fake, fake, fake, fake, -1, 4, 0, None) == S.LMBP_ERR_SHAPE
+    assert L.reswiglu2_fwd(fake, None, fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
+    assert L.reswiglu2_fwd(fake, fake, fake, fake, fake, 2, 4, 5, None) == S.LMBP_ERR_DTYPE
+    assert L.reswiglu2_bwd(fake, fake, fake, None, fake, fake, 2, 4, 1, None) == S.LMBP_ERR_NULLPTR
+    assert L.reswiglu2_bwd(fake, fake, fake, fake, fake, fake, 2, 0, 1, None) == S.LMBP_ERR_SHAPE
+    assert L.reswiglu2_bwd(None, None, None, None, None, None, 0, 4, 1, None) == S.LMBP_OK
     t = (ctypes.c_float * 4)()
     assert L.lmbp_step_table(5, ctypes.addressof(t), ctypes.addressof(t)) == S.LMBP_ERR_KIND
     assert L.lmbp_step_table(0, None, ctypes.addressof(t)) == S.LMBP_ERR_NULLPTR

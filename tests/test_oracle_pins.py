@@ -483,3 +483,59 @@ def test_tail_interval_examples():
         # the oracle's primitive really is below the bound beyond B
         f = oracle.gelu if ex["kind"] == "gelu" else oracle.silu
         assert abs(f(-B)) < 1 and abs(f(B) - B) < 1
+
+
+# --------------------------------------------------------------------------
+# ReSwiGLU2: SwiGLU gate with ReSiLU2
+# --------------------------------------------------------------------------
+def test_reswiglu2_matches_torch_autograd():
+    """Forward = torch float64 SiLU(g)*u; du = autograd wrt u; dg = autograd
+    of h~(g)*u with h~ the Eq. 14 ReLU combination written in torch (its
+    derivative is the step function away from the kinks)."""
+    rng = np.random.default_rng(12)
+    n = 4000
+    g = rng.normal(size=n) * 4
+    u = rng.normal(size=n)
+    dh = rng.normal(size=n)
+    c, s, a = oracle.step_table("silu")
+    g = g[np.min(np.abs(g[:, None] - c[None, :]), axis=1) > 1e-6]      # away from kinks
+    n = g.size
+    u, dh = u[:n], dh[:n]
+    h, act, codes = oracle.reswiglu2_fwd(g, u)
+    gt = torch.tensor(g, requires_grad=True)
+    ut = torch.tensor(u, requires_grad=True)
+    ht = torch.nn.functional.silu(gt) * ut
+    assert np.allclose(h, ht.detach().numpy(), rtol=1e-14, atol=1e-300)
+    assert np.allclose(act, torch.nn.functional.silu(gt).detach().numpy(), rtol=1e-14, atol=1e-300)
+    ht.backward(torch.tensor(dh))
+    w = [a[0], a[1], 1.0 - a[0] - a[1]]
+    g2 = torch.tensor(g, requires_grad=True)
+    ht2 = sum(wi * torch.relu(g2 - ci) for wi, ci in zip(w, c)) * torch.tensor(u)
+    ht2.backward(torch.tensor(dh))
+    dg, du = oracle.reswiglu2_bwd(dh, u, act, codes)
+    assert np.allclose(du, ut.grad.numpy(), rtol=1e-14, atol=1e-300)
+    assert np.allclose(dg, g2.grad.numpy(), rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_reswiglu2_contract_matches_torch_composition(dtype):
+    """Contract = torch's own unfused composition: da = (dh*u) rounded to T,
+    dg = (da.float() * RN32(s)) rounded to T, du = (dh*a) rounded to T."""
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[dtype]
+    rng = np.random.default_rng(13)
+    n = 5000
+    dh = torch.from_numpy(rng.normal(size=n)).to(tdt)
+    u = torch.from_numpy(rng.normal(size=n) * 3).to(tdt)
+    a = torch.from_numpy(rng.normal(size=n)).to(tdt)
+    cvals = rng.integers(0, 4, size=n)
+    packed = np.zeros((n + 3) // 4, dtype=np.uint8)
+    np.bitwise_or.at(packed, np.arange(n) // 4, (cvals << (2 * (np.arange(n) % 4))).astype(np.uint8))
+    _, s, _ = oracle.step_table("silu")
+    lv = torch.tensor(s).float()[torch.from_numpy(cvals)]
+    da = (dh.float() * u.float()).to(tdt)
+    want_dg = (da.float() * lv).to(tdt)
+    want_du = (dh.float() * a.float()).to(tdt)
+    st = (lambda t: t.view(torch.int16).numpy().view(np.uint16)) if dtype == "bf16" else (lambda t: t.numpy())
+    dg, du = oracle.reswiglu2_bwd_contract(st(dh), st(u), st(a), packed, dtype)
+    assert np.array_equal(dg.view(np.uint8), st(want_dg).view(np.uint8))
+    assert np.array_equal(du.view(np.uint8), st(want_du).view(np.uint8))
