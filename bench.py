@@ -248,7 +248,7 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
     n = gate.numel()
     h, a = torch.empty_like(gate), torch.empty_like(gate)
     codes = torch.empty(P.codes_bytes(n), dtype=torch.uint8, device=gate.device)
-    dh = up  # any [R, F] tensor in HBM
+    dh = torch.empty_like(up).copy_(gate).neg_()  # a third, distinct [R, F] tensor (no L2 sharing with up)
     dg, du = torch.empty_like(gate), torch.empty_like(gate)
     a2 = torch.empty_like(gate)
     fused = {

@@ -67,7 +67,8 @@ typedef enum {
   LMBP_ERR_DTYPE = 3,
   LMBP_ERR_EPS = 4,
   LMBP_ERR_CUDA = 5,
-  LMBP_ERR_KIND = 6
+  LMBP_ERR_KIND = 6,
+  LMBP_ERR_TABLE = 7
 } lmbp_status;
 
 typedef enum { LMBP_GELU = 0, LMBP_SILU = 1 } lmbp_act_kind;
@@ -176,6 +177,33 @@ LMBP_API int reswiglu2_fwd(const void *gate, const void *up, void *h, void *a, u
                            int64_t cols, int dtype, void *stream);
 LMBP_API int reswiglu2_bwd(const void *dh, const void *up, const void *a, const uint8_t *codes, void *dgate,
                            void *dup, int64_t rows, int64_t cols, int dtype, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Table-driven k-bit step activations: Eq. 14 with
+ * 2^k - 1 ReLUs, whose derivative is a 2^k-segment step function
+ * needing k bits per element (Prop. 4.1); "a larger k ... is also
+ * feasible".  k = 2 with the published tables reproduces
+ * regelu2_* / resilu2_* bitwise; other tables give e.g. ReGELU2-d (App. I,
+ * P:L1333-1351).
+ * Forward:  y = GELU(x) or SiLU(x) (act = LMBP_GELU / LMBP_SILU, unchanged
+ *           primitive); code = #{i : x > thresholds[i]}, i < 2^k - 1.
+ *           thresholds: HOST pointer to 2^k - 1 finite, strictly increasing
+ *           binary64 values; the library compares x > RD32(threshold), exact
+ *           for every fp32/bf16/fp16 x (reading R2).
+ * Backward: dx = RN_dtype(RN32(dy * RN32(levels[code])));
+ *           levels: HOST pointer to 2^k finite binary64 values.
+ * codes: lmbp_codes_bytes_k(rows*cols, k) = ceil(n k / 8) bytes; element j
+ *        at bits k*j .. k*j+k-1 of the LSB-first bit stream;
+ *        trailing bits of the last byte written as 0.
+ * k must be 1, 2 or 4 (else LMBP_ERR_TABLE, as for a malformed table).
+ * Layout, alignment (any; 16-byte aligned tensors take the vector path with
+ * identical results), aliasing and the other errors as above.
+ * ------------------------------------------------------------------------- */
+LMBP_API size_t lmbp_codes_bytes_k(int64_t n, int k);
+LMBP_API int stepact_fwd(int act, int k, const double *thresholds, const void *x, void *y, uint8_t *codes,
+                         int64_t rows, int64_t cols, int dtype, void *stream);
+LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint8_t *codes, void *dx,
+                         int64_t rows, int64_t cols, int dtype, void *stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

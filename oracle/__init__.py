@@ -77,6 +77,12 @@ def lib():
             f = getattr(L, name)
             f.restype, f.argtypes = i32, [p, p, p, i64, i64, p, i32]
         L.oracle_max_threads.restype, L.oracle_max_threads.argtypes = i32, []
+        L.oracle_stepact_fwd.restype = i32
+        L.oracle_stepact_fwd.argtypes = [i32, i32, p, p, i64, p, p]
+        L.oracle_stepact_bwd.restype = i32
+        L.oracle_stepact_bwd.argtypes = [i32, p, p, p, i64, p]
+        L.oracle_regelu2d_table.restype = i32
+        L.oracle_regelu2d_table.argtypes = [p, p]
         L.oracle_reswiglu2_fwd.restype = i32
         L.oracle_reswiglu2_fwd.argtypes = [p, p, i64, p, p, p, i32]
         L.oracle_reswiglu2_bwd.restype = i32
@@ -289,6 +295,53 @@ def msrms_bwd(dy64, y64, rstd64, nthreads=None):
     if R:
         assert lib().oracle_msrms_bwd(_ptr(dy), _ptr(y), _ptr(rstd), R, H, _ptr(dx), _nt(nthreads)) == 0
     return dx
+
+
+# --------------------------------------------------------------------------
+# k-bit step activations
+# --------------------------------------------------------------------------
+def codes_bytes_k(n: int, k: int) -> int:
+    return (int(n) * int(k) + 7) // 8
+
+
+def regelu2d_table():
+    """(c[3], s[4]) of ReGELU2-d, App. I."""
+    c, s = np.zeros(3), np.zeros(4)
+    lib().oracle_regelu2d_table(_ptr(c), _ptr(s))
+    return c, s
+
+
+def stepact_fwd(kind, k, thresholds, x64):
+    x = np.ascontiguousarray(x64, dtype=np.float64).reshape(-1)
+    c = np.ascontiguousarray(thresholds, dtype=np.float64)
+    if c.size != (1 << k) - 1:
+        raise ValueError("need 2^k - 1 thresholds")
+    n = x.size
+    y = np.empty(n)
+    codes = np.zeros(codes_bytes_k(n, k), dtype=np.uint8)
+    if n:
+        assert lib().oracle_stepact_fwd(_kind(kind), k, _ptr(c), _ptr(x), n, _ptr(y), _ptr(codes)) == 0
+    return y.reshape(np.shape(x64)), codes
+
+
+def stepact_bwd(k, levels, codes, dy64):
+    dy = np.ascontiguousarray(dy64, dtype=np.float64).reshape(-1)
+    s = np.ascontiguousarray(levels, dtype=np.float64)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = dy.size
+    if s.size != (1 << k) or codes.size != codes_bytes_k(n, k):
+        raise ValueError("table / codes size")
+    dx = np.empty(n)
+    if n:
+        assert lib().oracle_stepact_bwd(k, _ptr(s), _ptr(codes), _ptr(dy), n, _ptr(dx)) == 0
+    return dx.reshape(np.shape(dy64))
+
+
+def stepact_bwd_contract(k, levels, codes, dy_stored, dtype):
+    """RN_T(RN32(dy * RN32(level))) -- the binary32 product is exact in binary64."""
+    s32 = np.asarray(levels, dtype=np.float64).astype(np.float32).astype(np.float64)
+    prod = stepact_bwd(k, s32, codes, decode(dy_stored, dtype))
+    return round_to(prod, dtype).reshape(np.shape(dy_stored))
 
 
 # --------------------------------------------------------------------------

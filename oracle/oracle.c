@@ -319,6 +319,54 @@ int oracle_reswiglu2_bwd(const double *dh, const double *u, const double *a, con
     return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* k-bit step activations: Eq. 14 with 2^k - 1 ReLUs  */
+/* (P:L353-362); derivative = 2^k-segment step (Prop. 4.1).          */
+/* code = #{i : x > c_i}; packed k bits per element, element j at bits       */
+/* k*j .. k*j+k-1 of the LSB-first stream, trailing bits zero.      */
+/* ------------------------------------------------------------------------ */
+int oracle_stepact_fwd(int kind, int k, const double *c, const double *x, int64_t n, double *y, uint8_t *codes)
+{
+    if (k != 1 && k != 2 && k != 4) return -1;
+    int nt = (1 << k) - 1;
+    int64_t nbytes = (n * k + 7) / 8;
+    for (int64_t b = 0; b < nbytes; ++b) codes[b] = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        y[j] = (kind == ORACLE_GELU) ? oracle_gelu(x[j]) : oracle_silu(x[j]);
+        unsigned code = 0;
+        for (int i = 0; i < nt; ++i) code += (unsigned)(x[j] > c[i]);
+        int64_t bit = (int64_t)k * j;
+        codes[bit / 8] |= (uint8_t)(code << (bit % 8));
+    }
+    return 0;
+}
+
+int oracle_stepact_bwd(int k, const double *s, const uint8_t *codes, const double *dy, int64_t n, double *dx)
+{
+    if (k != 1 && k != 2 && k != 4) return -1;
+    unsigned mask = (1u << k) - 1u;
+    for (int64_t j = 0; j < n; ++j) {
+        int64_t bit = (int64_t)k * j;
+        unsigned code = (codes[bit / 8] >> (bit % 8)) & mask;
+        dx[j] = s[code] * dy[j];
+    }
+    return 0;
+}
+
+/* ReGELU2-d (App. I): the derivative-L2 fit of GELU. */
+static const double GELUD_A[2] = {0.32465931184406527, 0.34812875668739607};
+static const double GELUD_C[3] = {-0.4535743722857079, -0.0010587205574873046, 0.4487575313884231};
+
+int oracle_regelu2d_table(double c[3], double s[4])
+{
+    for (int i = 0; i < 3; ++i) c[i] = GELUD_C[i];
+    s[0] = 0.0;
+    s[1] = GELUD_A[0];
+    s[2] = GELUD_A[0] + GELUD_A[1];
+    s[3] = 1.0;
+    return 0;
+}
+
 /* Number of OpenMP threads a parallel region would use (for reporting). */
 int oracle_max_threads(void)
 {

@@ -28,10 +28,14 @@ SIGNATURES = {
     "msrms_fwd": (_i32, [_p, _p, _p, _i64, _i64, _f32, _i32, _p]),
     "msrms_bwd": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "reswiglu2_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "lmbp_codes_bytes_k": (ctypes.c_size_t, [_i64, _i32]),
+    "stepact_fwd": (_i32, [_i32, _i32, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "stepact_bwd": (_i32, [_i32, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "reswiglu2_bwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
 }
 
-LMBP_OK, LMBP_ERR_NULLPTR, LMBP_ERR_SHAPE, LMBP_ERR_DTYPE, LMBP_ERR_EPS, LMBP_ERR_CUDA, LMBP_ERR_KIND = range(7)
+(LMBP_OK, LMBP_ERR_NULLPTR, LMBP_ERR_SHAPE, LMBP_ERR_DTYPE, LMBP_ERR_EPS, LMBP_ERR_CUDA, LMBP_ERR_KIND,
+ LMBP_ERR_TABLE) = range(8)
 LMBP_F32, LMBP_BF16, LMBP_F16 = 0, 1, 2
 LMBP_GELU, LMBP_SILU = 0, 1
 

@@ -90,11 +90,62 @@ static int swiglu_bwd_entry(const void *dh, const void *u, const void *a, const 
   return status_of(swiglu_bwd(dtype, dh, u, a, codes, dg, du, rows * cols, static_cast<cudaStream_t>(stream)));
 }
 
+static bool k_ok(int k) { return k == 1 || k == 2 || k == 4; }
+
+// Round a binary64 threshold toward -inf into binary32 (reading R2).
+static float rd32(double c) {
+  float f = (float)c;
+  if ((double)f > c) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+
+static int stepact_fwd_entry(int act, int k, const double *thr, const void *x, void *y, uint8_t *codes,
+                             int64_t rows, int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (act != LMBP_GELU && act != LMBP_SILU) return LMBP_ERR_KIND;
+  if (!k_ok(k)) return LMBP_ERR_TABLE;
+  if (!thr) return LMBP_ERR_NULLPTR;
+  StepTable t{};
+  t.k = k;
+  for (int i = 0; i < (1 << k) - 1; ++i) {
+    if (!std::isfinite(thr[i]) || (i > 0 && !(thr[i] > thr[i - 1]))) return LMBP_ERR_TABLE;
+    t.thr[i] = rd32(thr[i]);
+  }
+  if (rows == 0) return LMBP_OK;
+  if (!x || !y || !codes) return LMBP_ERR_NULLPTR;
+  return status_of(stepact_fwd(act, dtype, t, x, y, codes, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
+static int stepact_bwd_entry(int k, const double *lvl, const void *dy, const uint8_t *codes, void *dx, int64_t rows,
+                             int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = check_dtype(dtype)) != LMBP_OK) return st;
+  if (!k_ok(k)) return LMBP_ERR_TABLE;
+  if (!lvl) return LMBP_ERR_NULLPTR;
+  StepTable t{};
+  t.k = k;
+  for (int i = 0; i < (1 << k); ++i) {
+    if (!std::isfinite(lvl[i])) return LMBP_ERR_TABLE;
+    t.lvl[i] = (float)lvl[i];
+  }
+  if (rows == 0) return LMBP_OK;
+  if (!dy || !dx || !codes) return LMBP_ERR_NULLPTR;
+  return status_of(stepact_bwd(dtype, t, dy, codes, dx, rows * cols, static_cast<cudaStream_t>(stream)));
+}
+
 }  // namespace lmbp
 
 extern "C" {
 
 size_t lmbp_codes_bytes(int64_t n) { return n <= 0 ? 0 : (size_t)((n + 3) / 4); }
+
+size_t lmbp_codes_bytes_k(int64_t n, int k) {
+  if (n <= 0 || !lmbp::k_ok(k)) return 0;
+  return (size_t)((n * k + 7) / 8);
+}
 
 const char *lmbp_status_string(int status) {
   switch (status) {
@@ -105,6 +156,7 @@ const char *lmbp_status_string(int status) {
     case LMBP_ERR_EPS: return "LMBP_ERR_EPS: eps must be finite and > 0";
     case LMBP_ERR_CUDA: return "LMBP_ERR_CUDA: kernel launch failed (cudaGetLastError)";
     case LMBP_ERR_KIND: return "LMBP_ERR_KIND: unknown activation kind";
+    case LMBP_ERR_TABLE: return "LMBP_ERR_TABLE: k not in {1, 2, 4}, or thresholds not finite and strictly increasing, or levels not finite";
     default: return "LMBP: unknown status";
   }
 }
@@ -162,6 +214,15 @@ int reswiglu2_fwd(const void *gate, const void *up, void *h, void *a, uint8_t *c
 int reswiglu2_bwd(const void *dh, const void *up, const void *a, const uint8_t *codes, void *dgate, void *dup,
                   int64_t rows, int64_t cols, int dtype, void *stream) {
   return lmbp::swiglu_bwd_entry(dh, up, a, codes, dgate, dup, rows, cols, dtype, stream);
+}
+
+int stepact_fwd(int act, int k, const double *thresholds, const void *x, void *y, uint8_t *codes, int64_t rows,
+                int64_t cols, int dtype, void *stream) {
+  return lmbp::stepact_fwd_entry(act, k, thresholds, x, y, codes, rows, cols, dtype, stream);
+}
+int stepact_bwd(int k, const double *levels, const void *dy, const uint8_t *codes, void *dx, int64_t rows,
+                int64_t cols, int dtype, void *stream) {
+  return lmbp::stepact_bwd_entry(k, levels, dy, codes, dx, rows, cols, dtype, stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,173 @@
+// stepact.cu -- table-driven k-bit step-derivative activations
+// (SURVEY.md 8(f) NEXT #3).
+//
+// Eq. 14 with 2^k - 1 ReLUs: the forward keeps the primitive
+// h = GELU or SiLU unchanged, the backward uses the 2^k-segment step function
+// dh~ (Prop. 4.1), so k bits per element are stored (P:L362,
+// "k is the required bit number").  k = 2 with the published tables is
+// ReGELU2 / ReSiLU2 (bitwise identical to regelu2_* / resilu2_*, tested);
+// other tables cover ReGELU2-d (App. I) and k = 1 / 4 variants
+// ("setting a larger k ... is also feasible").
+//
+// Packing: element j occupies bits k*j .. k*j + k - 1 of the flat
+// LSB-first bit stream, i.e. byte (k*j) / 8 at shift (k*j) % 8 (k | 8).
+// A thread owns groups of 8 elements = k bytes of codes.
+#include "act_math.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lmbp {
+
+template <int K>
+__device__ __forceinline__ uint32_t step_code(float x, const float *thr) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < (1 << K) - 1; ++i) c += (uint32_t)(x > thr[i]);
+  return c;
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T *p, int64_t g, bool vec, float *f) {
+  if (vec) {
+    if constexpr (Traits<T>::kVec == 8) {
+      Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + g), f);
+    } else {
+      Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + 2 * g), f);
+      Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + 2 * g + 1), f + 4);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = to_f32<T>(p[8 * g + e]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store8(T *p, int64_t g, bool vec, const float *f) {
+  if (vec) {
+    if constexpr (Traits<T>::kVec == 8) {
+      st_stream(reinterpret_cast<uint4 *>(p) + g, Vec<T>::pack(f));
+    } else {
+      st_stream(reinterpret_cast<uint4 *>(p) + 2 * g, Vec<T>::pack(f));
+      st_stream(reinterpret_cast<uint4 *>(p) + 2 * g + 1, Vec<T>::pack(f + 4));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) p[8 * g + e] = from_f32<T>(f[e]);
+  }
+}
+
+template <typename T, int A, bool kPrecise, int K>
+__global__ void __launch_bounds__(256) stepact_fwd_k(const T *x, T *y, uint8_t *codes, int64_t n, StepTable tab,
+                                                     bool vec) {
+  const int64_t groups = n / 8;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    load8<T>(x, g, vec, f);
+    uint32_t w = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      w |= step_code<K>(f[e], tab.thr) << (K * e);
+      f[e] = act_f<A, kPrecise>(f[e]);
+    }
+    store8<T>(y, g, vec, f);
+#pragma unroll
+    for (int b = 0; b < K; ++b) codes[g * K + b] = (uint8_t)(w >> (8 * b));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && groups * 8 < n) {  // ragged tail, trailing bits 0
+    uint32_t w = 0;
+    for (int64_t j = groups * 8; j < n; ++j) {
+      const float f = to_f32<T>(x[j]);
+      w |= step_code<K>(f, tab.thr) << (K * (j - groups * 8));
+      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+    }
+    const int nbytes = (int)(((n - groups * 8) * K + 7) / 8);
+    for (int b = 0; b < nbytes; ++b) codes[groups * K + b] = (uint8_t)(w >> (8 * b));
+  }
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256) stepact_bwd_k(const T *dy, const uint8_t *codes, T *dx, int64_t n,
+                                                     StepTable tab, bool vec) {
+  __shared__ float lvl[16];
+  if (threadIdx.x < (1 << K)) lvl[threadIdx.x] = tab.lvl[threadIdx.x];
+  __syncthreads();
+  constexpr uint32_t kMask = (1u << K) - 1u;
+  const int64_t groups = n / 8;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    load8<T>(dy, g, vec, f);
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b) w |= (uint32_t)codes[g * K + b] << (8 * b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = __fmul_rn(f[e], lvl[(w >> (K * e)) & kMask]);
+    store8<T>(dx, g, vec, f);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int64_t j = groups * 8; j < n; ++j) {
+      const int64_t bit = K * j;
+      const uint32_t c = (codes[bit >> 3] >> (bit & 7)) & kMask;
+      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), lvl[c]));
+    }
+  }
+}
+
+static int step_grid(int64_t groups) {
+  const int64_t want = (groups + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
+}
+
+template <typename T, int A, int K>
+static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, const StepTable &tab,
+                                 cudaStream_t s) {
+  constexpr bool kPrecise = std::is_same<T, float>::value;
+  const bool vec = (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
+  stepact_fwd_k<T, A, kPrecise, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(x),
+                                                                     reinterpret_cast<T *>(y), codes, n, tab, vec);
+  return cudaGetLastError();
+}
+
+template <typename T, int K>
+static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx, int64_t n, const StepTable &tab,
+                                 cudaStream_t s) {
+  const bool vec = (uintptr_t)dy % 16 == 0 && (uintptr_t)dx % 16 == 0;
+  stepact_bwd_k<T, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(dy), codes,
+                                                        reinterpret_cast<T *>(dx), n, tab, vec);
+  return cudaGetLastError();
+}
+
+template <typename T, int A>
+static cudaError_t fwd_k(int k, const void *x, void *y, uint8_t *codes, int64_t n, const StepTable &t, cudaStream_t s) {
+  if (k == 1) return stepact_fwd_t<T, A, 1>(x, y, codes, n, t, s);
+  if (k == 2) return stepact_fwd_t<T, A, 2>(x, y, codes, n, t, s);
+  return stepact_fwd_t<T, A, 4>(x, y, codes, n, t, s);
+}
+
+template <typename T>
+static cudaError_t bwd_k(int k, const void *dy, const uint8_t *codes, void *dx, int64_t n, const StepTable &t,
+                         cudaStream_t s) {
+  if (k == 1) return stepact_bwd_t<T, 1>(dy, codes, dx, n, t, s);
+  if (k == 2) return stepact_bwd_t<T, 2>(dy, codes, dx, n, t, s);
+  return stepact_bwd_t<T, 4>(dy, codes, dx, n, t, s);
+}
+
+cudaError_t stepact_fwd(int act, int dtype, const StepTable &t, const void *x, void *y, uint8_t *codes, int64_t n,
+                        cudaStream_t s) {
+  if (act == kActGelu) {
+    if (dtype == 0) return fwd_k<float, kActGelu>(t.k, x, y, codes, n, t, s);
+    if (dtype == 1) return fwd_k<__nv_bfloat16, kActGelu>(t.k, x, y, codes, n, t, s);
+    return fwd_k<__half, kActGelu>(t.k, x, y, codes, n, t, s);
+  }
+  if (dtype == 0) return fwd_k<float, kActSilu>(t.k, x, y, codes, n, t, s);
+  if (dtype == 1) return fwd_k<__nv_bfloat16, kActSilu>(t.k, x, y, codes, n, t, s);
+  return fwd_k<__half, kActSilu>(t.k, x, y, codes, n, t, s);
+}
+
+cudaError_t stepact_bwd(int dtype, const StepTable &t, const void *dy, const uint8_t *codes, void *dx, int64_t n,
+                        cudaStream_t s) {
+  if (dtype == 0) return bwd_k<float>(t.k, dy, codes, dx, n, t, s);
+  if (dtype == 1) return bwd_k<__nv_bfloat16>(t.k, dy, codes, dx, n, t, s);
+  return bwd_k<__half>(t.k, dy, codes, dx, n, t, s);
+}
+
+}  // namespace lmbp

@@ -198,3 +198,52 @@ def reswiglu2_bwd(dh, up, a, codes, dgate=None, dup=None, stream=None):
                                                dgate.data_ptr(), dup.data_ptr(), rows, cols, _dtype(dh),
                                                _stream(stream)))
     return dgate, dup
+
+
+# ---------------------------------------------------------------------------
+# k-bit step activations (lmbp.h stepact_*)
+# ---------------------------------------------------------------------------
+def codes_bytes_k(n: int, k: int) -> int:
+    return int(lib().lmbp_codes_bytes_k(int(n), int(k)))
+
+
+def _dbl(vals):
+    import ctypes
+    arr = (ctypes.c_double * len(vals))(*[float(v) for v in vals])
+    return arr, ctypes.addressof(arr)
+
+
+def stepact_fwd(x, act: str, k: int, thresholds, y=None, codes=None, stream=None):
+    """Forward of a k-bit step activation: (y = act(x), k-bit codes)."""
+    _need(x, "x")
+    n = x.numel()
+    y = torch.empty_like(x) if y is None else _need(y, "y")
+    codes = (torch.empty(codes_bytes_k(n, k), dtype=torch.uint8, device=x.device) if codes is None
+             else _need(codes, "codes"))
+    if y.shape != x.shape or y.dtype != x.dtype or codes.numel() != codes_bytes_k(n, k):
+        raise ValueError("stepact_fwd: shape/dtype/codes mismatch")
+    rows, cols = _rc(x)
+    keep, ptr = _dbl(thresholds)
+    if n == 0:
+        return y, codes
+    check("stepact_fwd", lib().stepact_fwd({"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}[act], int(k), ptr,
+                                           x.data_ptr(), y.data_ptr(), codes.data_ptr(), rows, cols, _dtype(x),
+                                           _stream(stream)))
+    return y, codes
+
+
+def stepact_bwd(dy, codes, k: int, levels, dx=None, stream=None):
+    """Backward of a k-bit step activation: dx = dy * levels[code]."""
+    _need(dy, "dy")
+    _need(codes, "codes")
+    n = dy.numel()
+    dx = torch.empty_like(dy) if dx is None else _need(dx, "dx")
+    if codes.numel() != codes_bytes_k(n, k) or dx.shape != dy.shape or dx.dtype != dy.dtype:
+        raise ValueError("stepact_bwd: shape/codes mismatch")
+    rows, cols = _rc(dy)
+    keep, ptr = _dbl(levels)
+    if n == 0:
+        return dx
+    check("stepact_bwd", lib().stepact_bwd(int(k), ptr, dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols,
+                                           _dtype(dy), _stream(stream)))
+    return dx

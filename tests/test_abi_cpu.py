@@ -59,7 +59,7 @@ def test_step_table_is_exact_rounding_of_paper_constants(kind):
 
 
 def test_status_strings():
-    for st in range(7):
+    for st in range(8):
         assert _lib.status_string(st).startswith("LMBP")
     assert "unknown" in _lib.status_string(99)
 
@@ -99,6 +99,19 @@ def test_validation_without_device_work():
     assert L.reswiglu2_bwd(fake, fake, fake, None, fake, fake, 2, 4, 1, None) == S.LMBP_ERR_NULLPTR
     assert L.reswiglu2_bwd(fake, fake, fake, fake, fake, fake, 2, 0, 1, None) == S.LMBP_ERR_SHAPE
     assert L.reswiglu2_bwd(None, None, None, None, None, None, 0, 4, 1, None) == S.LMBP_OK
+    good = (ctypes.c_double * 3)(-1.0, 0.0, 1.0)
+    bad = (ctypes.c_double * 3)(1.0, 0.0, 2.0)
+    lv = (ctypes.c_double * 4)(0.0, 0.1, 0.9, 1.0)
+    assert L.stepact_fwd(0, 3, ctypes.addressof(good), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
+    assert L.stepact_fwd(0, 2, ctypes.addressof(bad), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
+    assert L.stepact_fwd(9, 2, ctypes.addressof(good), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_KIND
+    assert L.stepact_fwd(0, 2, None, fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
+    assert L.stepact_fwd(0, 2, ctypes.addressof(good), None, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
+    assert L.stepact_bwd(2, ctypes.addressof(lv), fake, fake, fake, -1, 4, 0, None) == S.LMBP_ERR_SHAPE
+    assert L.stepact_bwd(5, ctypes.addressof(lv), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
+    assert L.stepact_bwd(2, ctypes.addressof(lv), None, None, None, 0, 4, 0, None) == S.LMBP_OK
+    for k, n in ((1, 9), (2, 9), (4, 9), (3, 9), (2, 0)):
+        assert L.lmbp_codes_bytes_k(n, k) == ((n * k + 7) // 8 if k in (1, 2, 4) else 0)
     t = (ctypes.c_float * 4)()
     assert L.lmbp_step_table(5, ctypes.addressof(t), ctypes.addressof(t)) == S.LMBP_ERR_KIND
     assert L.lmbp_step_table(0, None, ctypes.addressof(t)) == S.LMBP_ERR_NULLPTR
@@ -119,4 +132,6 @@ def test_product_package_does_not_import_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
-                assert "oracle" not in src.replace("oracle/", ""), f
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+                assert not re.search(r"#\s*include\s*[<\"].*oracle", src), f
+                assert "liboracle" not in src, f

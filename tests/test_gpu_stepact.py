@@ -1,0 +1,70 @@
+"""GPU parity for the table-driven k-bit step activations (SURVEY 8(f)
+NEXT #3): k = 2 with the published tables is bitwise identical to the
+specialised regelu2/resilu2 kernels; k = 1, 2 (ReGELU2-d), 4 against the
+oracle (codes bytewise, y within tolerance, dx bitwise to the contract)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2406_16282_b200 as P
+from paper_2406_16282_b200 import tables
+from test_gpu_parity import ATOL, DEV, RTOL, bits, dec, st
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("shape", [(1, 3), (3, 7), (37, 3072), (5, 1001)])
+def test_stepact_k2_paper_tables_equal_specialised(dtype, shape):
+    x = synth.act_input(*shape, dtype, mode="coverage").to(DEV)
+    dy = synth.grad_input(*shape, dtype).to(DEV)
+    for tab, fwd, bwd in ((tables.REGELU2, P.regelu2_fwd, P.regelu2_bwd),
+                          (tables.RESILU2, P.resilu2_fwd, P.resilu2_bwd)):
+        y1, c1 = P.stepact_fwd(x, tab["act"], 2, tab["c"])
+        y2, c2 = fwd(x)
+        dx1 = P.stepact_bwd(dy, c1, 2, tables.levels(tab))
+        dx2 = bwd(dy, c2)
+        torch.cuda.synchronize()
+        assert torch.equal(c1, c2)
+        assert st(y1).tobytes() == st(y2).tobytes()
+        assert st(dx1).tobytes() == st(dx2).tobytes()
+
+
+def _tables(k, rng):
+    if k == 1:
+        return [0.0], [0.0, 1.0]
+    if k == 2:
+        c, s = oracle.regelu2d_table()
+        return list(c), list(s)
+    c = sorted(rng.normal(size=15) * 3)
+    return c, list(rng.normal(size=16))
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", [(1, 5), (7, 33), (64, 3072)])
+def test_stepact_vs_oracle(k, dtype, shape):
+    rng = np.random.default_rng(k)
+    c, s = _tables(k, rng)
+    x = synth.act_input(*shape, dtype, mode="coverage")
+    dy = synth.grad_input(*shape, dtype)
+    y, codes = P.stepact_fwd(x.to(DEV), "gelu", k, c)
+    dx = P.stepact_bwd(dy.to(DEV), codes, k, s)
+    torch.cuda.synchronize()
+    x64 = dec(x, dtype)
+    y_ref, c_ref = oracle.stepact_fwd("gelu", k, c, x64)
+    assert np.array_equal(codes.cpu().numpy(), c_ref)
+    yr = y_ref.reshape(-1)
+    assert np.all(np.abs(dec(y, dtype).reshape(-1) - yr) <= RTOL[dtype] * np.abs(yr) + ATOL[dtype])
+    want = oracle.stepact_bwd_contract(k, s, c_ref, st(dy), dtype)
+    assert np.array_equal(bits(st(dx)), bits(want))
+
+
+def test_stepact_bad_tables():
+    x = torch.zeros(4, 8, device=DEV)
+    with pytest.raises(RuntimeError, match="TABLE"):
+        P.stepact_fwd(x, "gelu", 2, [1.0, 0.0, 2.0])           # not increasing
+    with pytest.raises(RuntimeError, match="TABLE"):
+        P.stepact_fwd(x, "gelu", 2, [0.0, float("nan"), 2.0])

@@ -539,3 +539,67 @@ def test_reswiglu2_contract_matches_torch_composition(dtype):
     dg, du = oracle.reswiglu2_bwd_contract(st(dh), st(u), st(a), packed, dtype)
     assert np.array_equal(dg.view(np.uint8), st(want_dg).view(np.uint8))
     assert np.array_equal(du.view(np.uint8), st(want_du).view(np.uint8))
+
+
+# --------------------------------------------------------------------------
+# k-bit step activations
+# --------------------------------------------------------------------------
+def _pack_k(codes, k):
+    out = np.zeros((len(codes) * k + 7) // 8, dtype=np.uint8)
+    for j, c in enumerate(codes):
+        out[(k * j) // 8] |= np.uint8(int(c) << ((k * j) % 8))
+    return out
+
+
+def test_stepact_k1_is_relu_derivative():
+    """k = 1, c = [0], s = (0, 1): the step derivative is ReLU' (closed form)."""
+    rng = np.random.default_rng(14)
+    x = rng.normal(size=1001)
+    dy = rng.normal(size=1001)
+    y, codes = oracle.stepact_fwd("gelu", 1, [0.0], x)
+    assert np.array_equal(codes, _pack_k((x > 0).astype(int), 1))
+    assert np.array_equal(oracle.stepact_bwd(1, [0.0, 1.0], codes, dy), dy * (x > 0))
+    assert np.allclose(y, [oracle.gelu(v) for v in x], rtol=0, atol=0)
+
+
+def test_stepact_k4_codes_are_searchsorted():
+    rng = np.random.default_rng(15)
+    c = np.sort(rng.normal(size=15) * 3)
+    x = np.concatenate([rng.normal(size=3000) * 4, c])          # incl. the kinks themselves
+    _, codes = oracle.stepact_fwd("silu", 4, c, x)
+    want = np.searchsorted(c, x, side="left")                    # #{i : c_i < x}
+    assert np.array_equal(codes, _pack_k(want, 4))
+    s = rng.normal(size=16)
+    dy = rng.normal(size=x.size)
+    assert np.array_equal(oracle.stepact_bwd(4, s, codes, dy), s[want] * dy)
+
+
+def test_stepact_k2_equals_regelu2_and_resilu2():
+    rng = np.random.default_rng(16)
+    x = rng.normal(size=2001) * 5
+    for kind in ("gelu", "silu"):
+        c, s, _ = oracle.step_table(kind)
+        y1, c1 = oracle.stepact_fwd(kind, 2, c, x)
+        y2, c2 = oracle.act_fwd(kind, x)
+        assert np.array_equal(c1, c2) and np.array_equal(y1, y2)
+        dy = rng.normal(size=x.size)
+        assert np.array_equal(oracle.stepact_bwd(2, s, c1, dy), oracle.act_bwd(kind, c2, dy))
+
+
+def test_regelu2d_table_from_paper():
+    """App. I constants typed in tests/golden; levels = slopes of Eq. 14 (FD);
+    the paper's own ReGELU2-d solution violates the Eq. 14 constraint by
+    ~7.9e-4 (derived; the derivative table does not depend on it)."""
+    c, s = oracle.regelu2d_table()
+    g = PAPER["gelu_d"]
+    assert list(c) == [float(v) for v in g["c"]]
+    a1, a2 = (float(v) for v in g["a"])
+    w = [a1, a2, 1.0 - a1 - a2]
+
+    def htilde(x):
+        return sum(wi * max(x - ci, 0.0) for wi, ci in zip(w, c))
+    mids = [c[0] - 1, 0.5 * (c[0] + c[1]), 0.5 * (c[1] + c[2]), c[2] + 1]
+    for kk, xm in enumerate(mids):
+        assert abs((htilde(xm + 1e-7) - htilde(xm - 1e-7)) / 2e-7 - s[kk]) < 1e-7
+    resid = sum(Fraction(wi) * Fraction(ci) for wi, ci in zip(w, c))
+    assert abs(float(resid) + 7.87e-4) < 1e-5
