@@ -292,6 +292,26 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
             "gpu_launches": 2 * iters}
 
 
+def block_section(cfg, R, dev):
+    """activation bytes an FFN half-block keeps for
+    backward (measured with saved_tensors_hooks, storage-deduplicated,
+    parameters excluded) -- exact reference (affine norm in fp32, exact
+    GELU/SiLU) vs ours (merged affine, MS norm, ReGELU2 / fused ReSwiGLU2) at
+    the config's shape; unit = one [R, H] 16-bit tensor (Fig. 2's unit)."""
+    from paper_2406_16282_b200.blocks import LlamaMLP, ViTMLP, activation_bytes
+    cls = ViTMLP if cfg["act"] == "gelu" else LlamaMLP
+    dt = synth.TORCH_DTYPES[cfg["dtype"]]
+    blk = cls(cfg["H"], cfg["F"], dtype=dt, device=dev)
+    x = synth.norm_input(R, cfg["H"], cfg["dtype"], device=dev).requires_grad_(True)
+    exact = activation_bytes(blk, x)
+    ours = activation_bytes(blk.to_ours(), x)
+    unit = R * cfg["H"] * 2
+    torch.cuda.synchronize()
+    return {"block": cls.__name__, "rows": R, "exact_bytes": exact, "ours_bytes": ours,
+            "saved_fraction": round(1 - ours / exact, 4), "exact_units": round(exact / unit, 3),
+            "ours_units": round(ours / unit, 3)}
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -476,6 +496,7 @@ def main():
                        f"round-robin on {len(streams)} streams (copies overlap kernels and each other)"}
 
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
+    block = block_section(cfg, R, dev) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -500,6 +521,7 @@ def main():
             "per_rank_ms": [round(m, 3) for m in ms_all],
             "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
             "reswiglu2": swiglu,
+            "activation_bytes_saved_per_block": block,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
