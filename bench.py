@@ -55,6 +55,7 @@ def parse(argv=None):
     ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the full config (its own batch); "
                          "strong: the config's rows are split across ranks")
@@ -172,6 +173,8 @@ def oracle_step_sample(cfg, rows, eps):
     """One oracle pass of the four rows of 8(a) on `rows` rows; returns
     (seconds, algorithmic bytes, threads)."""
     import oracle
+    if oracle.DEFAULT_THREADS is None:      # all usable host cores, whatever OMP_NUM_THREADS says
+        oracle.DEFAULT_THREADS = len(os.sched_getaffinity(0))
     dt = cfg["dtype"]
     x = synth.to_numpy_storage(synth.act_input(rows, cfg["F"], dt))
     dy = synth.to_numpy_storage(synth.grad_input(rows, cfg["F"], dt))
@@ -320,11 +323,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     world, rank, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    # one process per GPU; --dist-backend gloo (with ranks sharing a device via
+    # local % device_count) exists only to exercise the N > 1 path on one GPU.
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:
+            torch.distributed.init_process_group("gloo")
 
     import paper_2406_16282_b200 as P
 
@@ -389,7 +396,8 @@ def main():
     total_ms = sum(sum(v) for v in per_kernel.values())
     nbytes = algorithmic_bytes(cfg, R)
     step_bytes = sum(nbytes.values())
-    t = torch.tensor([total_ms, float(step_bytes)], dtype=torch.float64, device=dev)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([total_ms, float(step_bytes)], dtype=torch.float64, device=cdev)
     if world > 1:
         parts = [torch.zeros_like(t) for _ in range(world)]
         torch.distributed.all_gather(parts, t)
@@ -486,7 +494,7 @@ def main():
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=cdev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": round(sum(bytes_all) * args.e2e_steps / (te.item() / 1e3) / 1e9, 2), "unit": "GB/s",

@@ -100,7 +100,14 @@ def _kind(kind) -> int:
     return KINDS[kind] if isinstance(kind, str) else int(kind)
 
 
+# Threads the oracle uses when a call does not say (None = OpenMP's default,
+# which honours OMP_NUM_THREADS; bench.py sets it to the host's usable cores).
+DEFAULT_THREADS = None
+
+
 def max_threads() -> int:
+    if DEFAULT_THREADS is not None:
+        return int(DEFAULT_THREADS)
     return int(lib().oracle_max_threads())
 
 
