@@ -23,10 +23,9 @@
  *   j >> 2 at bits 2*(j & 3) (LSB first); the buffer holds
  *   exactly lmbp_codes_bytes(n) = ceil(n / 4) bytes and the unused high bits of
  *   the last byte are written as 0.
- * Alignment.  The vector path needs 16-byte aligned tensor pointers (and a
- *   2-byte aligned `codes` for 16-bit dtypes).  Anything else runs a scalar
- *   path with bitwise-identical activation results; misalignment is never an
- *   error.
+ * Alignment.  The vector (TMA) path needs 16-byte aligned tensor and `codes`
+ *   pointers.  Anything else runs a scalar path with bitwise-identical
+ *   activation results; misalignment is never an error.
  * Aliasing.  Exact aliasing y == x (forward) or dx == dy (backward) is
  *   allowed: every element / row is read before it is written.  Partial
  *   overlap is undefined.
@@ -168,8 +167,7 @@ LMBP_API int msrms_bwd(const void *dy, const void *y, const float *rstd, void *d
  *           dgate = RN_dtype(RN32(RN_dtype(RN32(dh * up)) * RN32(s[code])))
  *           dh, up, a: [rows, cols]; codes as written by reswiglu2_fwd;
  *           dgate, dup: [rows, cols] outputs.
- * Vector path: all tensor pointers 16-byte aligned (forward: codes 2-byte
- * aligned for 16-bit dtypes; backward: codes 16-byte aligned), else a scalar
+ * Vector path: all tensor and codes pointers 16-byte aligned, else a scalar
  * path with bitwise-identical results.  Any output may exactly alias any
  * input of the same shape.  Errors as above.
  * ------------------------------------------------------------------------- */

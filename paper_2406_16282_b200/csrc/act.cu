@@ -136,8 +136,9 @@ __global__ void __launch_bounds__(256) act_bwd_scalar(const T *dy, const uint8_t
 // forward 16 consumer warps x 2 vectors/lane (16 KB tiles) x 4 stages;
 // backward 12 warps x 4 vectors/lane (24 KB tiles + codes) x 3 stages.
 // ---------------------------------------------------------------------------
+// Returns the code word (forward); the caller stores it.
 template <typename T, int A, bool kPrecise, bool kFwd>
-__device__ __forceinline__ void act_vec_op(const uint4 &v, uint32_t c_in, uint4 *out, CodeWord<T> *cw, int64_t i) {
+__device__ __forceinline__ uint32_t act_vec_op(const uint4 &v, uint32_t c_in, uint4 *out, int64_t i) {
   constexpr int kVec = Traits<T>::kVec;
   float f[kVec];
   Vec<T>::unpack(v, f);
@@ -145,26 +146,35 @@ __device__ __forceinline__ void act_vec_op(const uint4 &v, uint32_t c_in, uint4 
     uint32_t c;
     if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
     else c = codes_vec_16<T, A>(v);
+#ifndef LMBP_DIAG_NO_MATH
 #pragma unroll
     for (int k = 0; k < kVec; k += 2) {
       const float2 r = act2_f<A, kPrecise>(make_float2(f[k], f[k + 1]));
       f[k] = r.x;
       f[k + 1] = r.y;
     }
+#endif
     st_stream(out + i, Vec<T>::pack(f));
-    cw[i] = (CodeWord<T>)c;
+    return c;
   } else {
 #pragma unroll
     for (int k = 0; k < kVec; ++k) f[k] = __fmul_rn(f[k], level<A>((c_in >> (2 * k)) & 3u));
     st_stream(out + i, Vec<T>::pack(f));
+    return 0u;
   }
 }
 
 template <typename T, int A, bool kPrecise>
+#ifndef LMBP_FWD_W
+#define LMBP_FWD_W 16
+#define LMBP_FWD_U 2
+#define LMBP_FWD_S 4
+#endif
 struct ActFwdOp {
-  static constexpr int W = 16, U = 2, S = 4, kIn = 1, kCodeIn = 0;
-  __device__ static void apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p) {
-    act_vec_op<T, A, kPrecise, true>(v[0], 0u, p.out[0], reinterpret_cast<CodeWord<T> *>(p.codes_out), i);
+  static constexpr int W = LMBP_FWD_W, U = LMBP_FWD_U, S = LMBP_FWD_S, kIn = 1, kCodeIn = 0;
+  static constexpr int kCodeOut = Traits<T>::kVec / 4;
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p) {
+    return act_vec_op<T, A, kPrecise, true>(v[0], 0u, p.out[0], i);
   }
   __device__ static void tail(const EwParams &p) {
     constexpr int kVec = Traits<T>::kVec;
@@ -184,9 +194,9 @@ __device__ void act_bwd_tail(const T *dy, const uint8_t *codes, T *dx, int64_t j
 
 template <typename T, int A>
 struct ActBwdOp {
-  static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = Traits<T>::kVec / 4;
-  __device__ static void apply(const uint4 (&v)[1], uint32_t c, int64_t i, const EwParams &p) {
-    act_vec_op<T, A, false, false>(v[0], c, p.out[0], nullptr, i);
+  static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = Traits<T>::kVec / 4, kCodeOut = 0;
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const EwParams &p) {
+    return act_vec_op<T, A, false, false>(v[0], c, p.out[0], i);
   }
   __device__ static void tail(const EwParams &p) {
     act_bwd_tail<T, A>(reinterpret_cast<const T *>(p.in[0]), p.codes_in, reinterpret_cast<T *>(p.out[0]),
@@ -213,8 +223,9 @@ template <typename T, int A>
 static cudaError_t act_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, cudaStream_t s) {
   constexpr int kVec = Traits<T>::kVec;
   constexpr bool kPrecise = std::is_same<T, float>::value;
-  const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
-                       (kVec == 4 || (uintptr_t)codes % 2 == 0);
+  // The TMA path writes each warp's codes as 16-byte vectors: codes must be
+  // 16-byte aligned too (any other alignment takes the scalar path).
+  const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && ((uintptr_t)codes % 16 == 0);
   const int sms = sm_count();
   if (aligned) {
     EwParams p{};

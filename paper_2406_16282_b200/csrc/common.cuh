@@ -211,6 +211,35 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Cluster launch control (sm_100): ask the hardware to cancel a CTA of this
+// grid that has not started yet; the response (16 bytes in shared memory)
+// arrives on `bar` with complete_tx.  Hardware work stealing without any
+// global counter (the library keeps no mutable global state).
+__device__ __forceinline__ void clc_try_cancel(void *resp, uint64_t *bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+          smem_u32(resp)),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+// Returns the x index of the cancelled CTA, or -1 when nothing was cancelled.
+__device__ __forceinline__ int clc_query(const void *resp) {
+  uint32_t ok, cx;
+  asm volatile(
+      "{\n"
+      ".reg .b128 r;\n"
+      ".reg .pred p;\n"
+      "ld.shared.b128 r, [%2];\n"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n"
+      "}\n"
+      : "=r"(ok), "=r"(cx)
+      : "r"(smem_u32(resp))
+      : "memory");
+  return ok ? (int)cx : -1;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));

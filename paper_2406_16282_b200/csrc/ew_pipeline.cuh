@@ -14,7 +14,9 @@
 //   static constexpr int W, U, S;   consumer warps, vectors per lane per tile, stages
 //   static constexpr int kIn;       input streams (1..3)
 //   static constexpr int kCodeIn;   bytes of packed codes read per vector (0, 1, 2)
-//   __device__ static void apply(const uint4 (&v)[kIn], uint32_t code, int64_t i, const EwParams &p);
+//   static constexpr int kCodeOut;  // bytes of packed codes written per vector (0, 1, 2)
+//   __device__ static uint32_t apply(const uint4 (&v)[kIn], uint32_t code, int64_t i, const EwParams &p);
+//       -> the code word of vector i (ignored when kCodeOut == 0)
 //   __device__ static void tail(const EwParams &p);   elements [nvec * kVec, n), one thread
 #pragma once
 
@@ -35,9 +37,22 @@ template <class Op> struct EwShape {
   static constexpr int kTile = Op::W * 32 * Op::U;  // vectors per tile
   static constexpr int kThreads = (Op::W + 1) * 32;
   static constexpr size_t kStageBytes = (size_t)Op::kIn * kTile * 16 + (size_t)Op::kCodeIn * kTile;
-  static constexpr size_t kSmem = (size_t)Op::S * kStageBytes + 2 * (size_t)Op::S * sizeof(uint64_t);
+  // per-warp staging of the codes a warp writes for one tile (32 U words)
+  static constexpr size_t kWarpCodeBytes = (size_t)32 * Op::U * Op::kCodeOut;
+  static constexpr size_t kCodeStage = (size_t)Op::W * kWarpCodeBytes;
+  // stages | code staging | full[S] empty[S] clc_bar (+pad) | slot[S+1] | clc response (16 B)
+  static constexpr size_t kBarBytes = (2 * (size_t)Op::S + 2) * sizeof(uint64_t);
+  static constexpr size_t kSlotBytes = (((size_t)Op::S + 1) * sizeof(int64_t) + 15) / 16 * 16;
+  static constexpr size_t kSmem = (size_t)Op::S * kStageBytes + kCodeStage + kBarBytes + kSlotBytes + 16;
   static_assert(kStageBytes % 16 == 0, "stage must stay 16-byte aligned");
+  static_assert(kWarpCodeBytes % 16 == 0, "code staging must stay 16-byte aligned");
 };
+
+template <int kCodeOut>
+__device__ __forceinline__ void put_code(uint8_t *base, int64_t i, uint32_t c) {
+  if constexpr (kCodeOut == 2) reinterpret_cast<uint16_t *>(base)[i] = (uint16_t)c;
+  else if constexpr (kCodeOut == 1) base[i] = (uint8_t)c;
+}
 
 template <int kCodeIn>
 __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
@@ -46,21 +61,40 @@ __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
   else return 0u;
 }
 
+// Tile schedule: hardware work stealing with cluster launch control.  The
+// grid has one CTA per work unit of kUnit consecutive tiles (+ one pseudo-tile
+// index == ntiles that stands for the leftover vectors and the ragged tail).
+// Each running CTA's producer lane asks the hardware (clusterlaunchcontrol.
+// try_cancel) for a not-yet-started CTA of the grid and takes over its unit,
+// so the block scheduler's dynamic balance is kept without paying a CTA
+// launch, barrier initialisation and pipeline ramp per unit.  The producer
+// tells the consumers which tile a stage holds through a per-stage slot
+// (written before the stage's mbarrier arrive, read after its wait); -1 ends.
+#ifndef LMBP_EW_UNIT
+#define LMBP_EW_UNIT 1
+#endif
+
 template <class Op>
 __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const EwParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Sh = EwShape<Op>;
   constexpr int W = Op::W, U = Op::U, S = Op::S, NIN = Op::kIn, TILE = Sh::kTile;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * Sh::kStageBytes);
+  uint8_t *cstage = smem + (size_t)S * Sh::kStageBytes;  // codes staging, one slice per warp
+  uint64_t *full = reinterpret_cast<uint64_t *>(cstage + Sh::kCodeStage);
   uint64_t *empty = full + S;
+  uint64_t *clc_bar = empty + S;
+  int64_t *slot = reinterpret_cast<int64_t *>(clc_bar + 2);   // tile index held by each stage
+  uint4 *clc_resp = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(slot) + Sh::kSlotBytes);  // 16 B aligned
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = p.nvec / TILE;
+  const int64_t nitems = ntiles + 1;                           // + the leftover pseudo-tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], W);
     }
+    mbar_init(clc_bar, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -68,52 +102,99 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const EwParams p
   if (warp == W) {  // producer
     if (lane == 0) {
       int k = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int s = k % S;
-        mbar_wait(&empty[s], ((uint32_t)(k / S) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], (uint32_t)Sh::kStageBytes);
-        uint8_t *st = smem + (size_t)s * Sh::kStageBytes;
+      int64_t unit = blockIdx.x;
+      uint32_t clc_phase = 0;
+      bool more = true;
+      while (more) {
+        // request the next unit now; the answer arrives while this unit streams
+        mbar_arrive_expect_tx(clc_bar, 16);
+        clc_try_cancel(clc_resp, clc_bar);
+        const int64_t t_end = min(nitems, (unit + 1) * LMBP_EW_UNIT);
+        for (int64_t t = unit * LMBP_EW_UNIT; t < t_end; ++t, ++k) {
+          const int s = k % S;
+          mbar_wait(&empty[s], ((uint32_t)(k / S) & 1u) ^ 1u);
+          slot[s] = t;
+          if (t == ntiles) {             // leftover pseudo-tile: nothing to load
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Sh::kStageBytes);
+          uint8_t *st = smem + (size_t)s * Sh::kStageBytes;
 #pragma unroll
-        for (int m = 0; m < NIN; ++m) bulk_g2s(st + (size_t)m * TILE * 16, p.in[m] + t * TILE, TILE * 16, &full[s]);
-        if constexpr (Op::kCodeIn > 0)
-          bulk_g2s(st + (size_t)NIN * TILE * 16, p.codes_in + t * TILE * Op::kCodeIn, TILE * Op::kCodeIn, &full[s]);
+          for (int m = 0; m < NIN; ++m) bulk_g2s(st + (size_t)m * TILE * 16, p.in[m] + t * TILE, TILE * 16, &full[s]);
+          if constexpr (Op::kCodeIn > 0)
+            bulk_g2s(st + (size_t)NIN * TILE * 16, p.codes_in + t * TILE * Op::kCodeIn, TILE * Op::kCodeIn,
+                     &full[s]);
+        }
+        mbar_wait(clc_bar, clc_phase);
+        clc_phase ^= 1u;
+        const int next = clc_query(clc_resp);
+        more = next >= 0;
+        unit = next;
       }
+      const int s = k % S;                 // end of stream
+      mbar_wait(&empty[s], ((uint32_t)(k / S) & 1u) ^ 1u);
+      slot[s] = -1;
+      mbar_arrive(&full[s]);
     }
     return;
   }
 
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+  for (int k = 0;; ++k) {
     const int s = k % S;
     mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
+    const int64_t t = slot[s];
+    if (t < 0) break;
+    if (t == ntiles) {
+      // Leftover vectors (< one tile) with direct loads, then the ragged tail.
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      for (int64_t i = ntiles * TILE + threadIdx.x; i < p.nvec; i += W * 32) {
+        uint4 v[NIN];
+#pragma unroll
+        for (int m = 0; m < NIN; ++m) v[m] = ld_stream(p.in[m] + i);
+        const uint32_t co = Op::apply(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p);
+        put_code<Op::kCodeOut>(p.codes_out, i, co);
+      }
+      if (threadIdx.x == 0) Op::tail(p);
+      continue;
+    }
     const uint8_t *st = smem + (size_t)s * Sh::kStageBytes;
+    // Warp w owns the contiguous vectors [w 32 U, (w + 1) 32 U) of the tile;
+    // each warp instruction still touches 512 contiguous bytes.
     uint4 v[U][NIN];
     uint32_t c[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int vi = j * (W * 32) + warp * 32 + lane;
+      const int vi = warp * (32 * U) + j * 32 + lane;
 #pragma unroll
       for (int m = 0; m < NIN; ++m) v[j][m] = lds128(st + ((size_t)m * TILE + vi) * 16);
       c[j] = code_word<Op::kCodeIn>(st + (size_t)NIN * TILE * 16, vi);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage may be refilled while we compute
+    const int64_t wbase = t * TILE + warp * (32 * U);
 #pragma unroll
-    for (int j = 0; j < U; ++j) Op::apply(v[j], c[j], t * TILE + j * (W * 32) + warp * 32 + lane, p);
-  }
-
-  if (blockIdx.x == 0) {  // leftover vectors (< one tile), then the ragged element tail
-    for (int64_t i = ntiles * TILE + threadIdx.x; i < p.nvec; i += W * 32) {
-      uint4 v[NIN];
-#pragma unroll
-      for (int m = 0; m < NIN; ++m) v[m] = ld_stream(p.in[m] + i);
-      Op::apply(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p);
+    for (int j = 0; j < U; ++j) {
+      const uint32_t co = Op::apply(v[j], c[j], wbase + j * 32 + lane, p);
+      if constexpr (Op::kCodeOut > 0) put_code<Op::kCodeOut>(cstage + warp * Sh::kWarpCodeBytes, j * 32 + lane, co);
     }
-    if (threadIdx.x == 0) Op::tail(p);
+    if constexpr (Op::kCodeOut > 0) {
+      // The warp's codes are one contiguous run of 32 U words: write them as
+      // full 16-byte vectors (whole 128-byte lines for 16-bit types) instead
+      // of 2-byte stores from every lane.
+      __syncwarp();
+      constexpr int kChunks = (int)(Sh::kWarpCodeBytes / 16);
+      if (lane < kChunks) {
+        const uint4 w = lds128(cstage + warp * Sh::kWarpCodeBytes + lane * 16);
+        st_stream(reinterpret_cast<uint4 *>(p.codes_out + wbase * Op::kCodeOut) + lane, w);
+      }
+      __syncwarp();
+    }
   }
 }
 
-// Launch on a persistent grid of SMs x resident CTAs (at most one CTA per tile).
+// Launch one CTA per work unit; resident CTAs steal the rest through CLC.
 template <class Op>
 cudaError_t launch_ew(const EwParams &p, cudaStream_t stream) {
   using Sh = EwShape<Op>;
@@ -125,8 +206,11 @@ cudaError_t launch_ew(const EwParams &p, cudaStream_t stream) {
       b = 1;
     return b;
   }();
-  const int64_t tiles = p.nvec / Sh::kTile;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * occ));
+  const int64_t items = p.nvec / Sh::kTile + 1;
+  const int64_t units = (items + LMBP_EW_UNIT - 1) / LMBP_EW_UNIT;
+  if (units > 0x7fffffff) return cudaErrorInvalidValue;
+  const int grid = (int)units;  // CTAs beyond the resident ones are taken over via CLC
+  (void)occ;
   kern<<<grid, Sh::kThreads, Sh::kSmem, stream>>>(p);
   return cudaGetLastError();
 }

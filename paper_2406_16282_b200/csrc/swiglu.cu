@@ -35,8 +35,8 @@ __device__ __forceinline__ void swiglu_bwd_elem(float dh, float u, float a, uint
 
 template <typename T, bool kPrecise>
 struct SwiGluFwdOp {
-  static constexpr int W = 16, U = 2, S = 3, kIn = 2, kCodeIn = 0;
-  __device__ static void apply(const uint4 (&v)[2], uint32_t, int64_t i, const EwParams &p) {
+  static constexpr int W = 16, U = 2, S = 3, kIn = 2, kCodeIn = 0, kCodeOut = Traits<T>::kVec / 4;
+  __device__ static uint32_t apply(const uint4 (&v)[2], uint32_t, int64_t i, const EwParams &p) {
     constexpr int kVec = Traits<T>::kVec;
     float g[kVec], u[kVec], a[kVec];
     Vec<T>::unpack(v[0], g);
@@ -56,7 +56,7 @@ struct SwiGluFwdOp {
     for (int k = 0; k < kVec; ++k) a[k] = __fmul_rn(a[k], u[k]);
     st_stream(p.out[0] + i, Vec<T>::pack(a));
     st_stream(p.out[1] + i, aT);
-    reinterpret_cast<CodeWord<T> *>(p.codes_out)[i] = (CodeWord<T>)c;
+    return c;
   }
   __device__ static void tail(const EwParams &p) {
     const T *g = reinterpret_cast<const T *>(p.in[0]);
@@ -79,8 +79,8 @@ struct SwiGluFwdOp {
 
 template <typename T>
 struct SwiGluBwdOp {
-  static constexpr int W = 12, U = 2, S = 3, kIn = 3, kCodeIn = Traits<T>::kVec / 4;
-  __device__ static void apply(const uint4 (&v)[3], uint32_t c, int64_t i, const EwParams &p) {
+  static constexpr int W = 12, U = 2, S = 3, kIn = 3, kCodeIn = Traits<T>::kVec / 4, kCodeOut = 0;
+  __device__ static uint32_t apply(const uint4 (&v)[3], uint32_t c, int64_t i, const EwParams &p) {
     constexpr int kVec = Traits<T>::kVec;
     float dh[kVec], u[kVec], a[kVec];
     Vec<T>::unpack(v[0], dh);
@@ -96,6 +96,7 @@ struct SwiGluBwdOp {
 #pragma unroll
     for (int k = 0; k < kVec; ++k) u[k] = __fmul_rn(u[k], level<kActSilu>((c >> (2 * k)) & 3u));
     st_stream(p.out[0] + i, Vec<T>::pack(u));
+    return 0u;
   }
   __device__ static void tail(const EwParams &p) {
     const T *dh = reinterpret_cast<const T *>(p.in[0]);
@@ -152,7 +153,7 @@ static cudaError_t swiglu_fwd_t(const void *g, const void *u, void *h, void *a, 
                                 cudaStream_t s) {
   constexpr int kVec = Traits<T>::kVec;
   constexpr bool kPrecise = std::is_same<T, float>::value;
-  if (al16(g) && al16(u) && al16(h) && al16(a) && (kVec == 4 || (uintptr_t)codes % 2 == 0)) {
+  if (al16(g) && al16(u) && al16(h) && al16(a) && al16(codes)) {
     EwParams p{};
     p.in[0] = reinterpret_cast<const uint4 *>(g);
     p.in[1] = reinterpret_cast<const uint4 *>(u);

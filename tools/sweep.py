@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--kernels", default="act_fwd,act_bwd,norm_fwd,norm_bwd")
     ap.add_argument("--build-only", action="store_true")
+    ap.add_argument("--yoff", type=int, default=0, help="offset y by this many bytes (address-interaction probe)")
     a = ap.parse_args()
     libs = {}
     for v in a.variants:
@@ -50,7 +51,9 @@ def main():
     dev = torch.device("cuda")
     x = synth.act_input(R, F, dt, device=dev)
     dy = synth.grad_input(R, F, dt, device=dev)
-    y, dx = torch.empty_like(x), torch.empty_like(dy)
+    ybuf = torch.empty(x.numel() * x.element_size() + a.yoff, dtype=torch.uint8, device=dev)
+    y = ybuf[a.yoff:].view(x.dtype).view(x.shape)
+    dx = torch.empty_like(dy)
     codes = torch.empty((R * F + 3) // 4, dtype=torch.uint8, device=dev)
     xn = synth.norm_input(R, H, dt, device=dev)
     gn = synth.grad_input(R, H, dt, device=dev)
@@ -94,7 +97,7 @@ def main():
             torch.cuda.synchronize()
             us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ts)
             med = us[len(us) // 2]
-            print(json.dumps({"variant": name, "config": a.config, "kernel": k, "us_med": round(med, 2),
+            print(json.dumps({"variant": name, "config": a.config, "kernel": k, "yoff": a.yoff, "us_med": round(med, 2),
                               "us_min": round(us[0], 2), "GB/s": round(nbytes[k] / med / 1e3, 1),
                               "frac": round(nbytes[k] / med / 1e3 / 6536, 4)}), flush=True)
 
