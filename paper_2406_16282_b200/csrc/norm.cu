@@ -294,34 +294,45 @@ __global__ void __launch_bounds__(512) norm_tma(const uint4 *a, const uint4 *b, 
       }
       if (lane == 0) rstd_out[row] = r;
     } else {
+      // Packed f32x2 math (FADD2/FFMA2/FMUL2) and four independent
+      // accumulator pairs: the ring kernel runs few warps per SM (the ring
+      // fills shared memory), so per-warp ILP decides its speed.
       const uint4 *sb = sa + nvec;
       const float r = rstd_in[row];
-      float g0 = 0.0f, g1 = 0.0f, p0 = 0.0f, p1 = 0.0f;
+      const float2 z2 = make_float2(0.0f, 0.0f);
+      float2 gs0 = z2, gs1 = z2, ps0 = z2, ps1 = z2;
+#pragma unroll 2
+      for (int vi = lane; vi < nvec; vi += 32) {
+        float g[kVec], h[kVec];
+        Vec<T>::unpack(lds128(sa + vi), g);
+        Vec<T>::unpack(lds128(sb + vi), h);
+#pragma unroll
+        for (int e = 0; e < kVec; e += 4) {
+          const float2 ga = make_float2(g[e], g[e + 1]), gb = make_float2(g[e + 2], g[e + 3]);
+          if constexpr (NORM == kNormLN) {
+            gs0 = __fadd2_rn(gs0, ga);
+            gs1 = __fadd2_rn(gs1, gb);
+          }
+          ps0 = __ffma2_rn(ga, make_float2(h[e], h[e + 1]), ps0);
+          ps1 = __ffma2_rn(gb, make_float2(h[e + 2], h[e + 3]), ps1);
+        }
+      }
+      const float2 acc = warp_sum2(make_float2((gs0.x + gs0.y) + (gs1.x + gs1.y), (ps0.x + ps0.y) + (ps1.x + ps1.y)));
+      const float m1 = NORM == kNormLN ? __fdiv_rn(acc.x, fcols) : 0.0f;
+      const float m2 = __fdiv_rn(acc.y, fcols);
+      const float2 nm1 = make_float2(-m1, -m1), nm2 = make_float2(-m2, -m2), r2 = make_float2(r, r);
+#pragma unroll 2
       for (int vi = lane; vi < nvec; vi += 32) {
         float g[kVec], h[kVec];
         Vec<T>::unpack(lds128(sa + vi), g);
         Vec<T>::unpack(lds128(sb + vi), h);
 #pragma unroll
         for (int e = 0; e < kVec; e += 2) {
-          if constexpr (NORM == kNormLN) {
-            g0 += g[e];
-            g1 += g[e + 1];
-          }
-          p0 = fmaf(g[e], h[e], p0);
-          p1 = fmaf(g[e + 1], h[e + 1], p1);
-        }
-      }
-      const float2 acc = warp_sum2(make_float2(g0 + g1, p0 + p1));
-      const float m1 = NORM == kNormLN ? __fdiv_rn(acc.x, fcols) : 0.0f;
-      const float m2 = __fdiv_rn(acc.y, fcols);
-      for (int vi = lane; vi < nvec; vi += 32) {
-        float g[kVec], h[kVec];
-        Vec<T>::unpack(lds128(sa + vi), g);
-        Vec<T>::unpack(lds128(sb + vi), h);
-#pragma unroll
-        for (int e = 0; e < kVec; ++e) {
-          const float c = NORM == kNormLN ? __fsub_rn(g[e], m1) : g[e];
-          g[e] = __fmul_rn(r, fmaf(-h[e], m2, c));
+          float2 c = make_float2(g[e], g[e + 1]);
+          if constexpr (NORM == kNormLN) c = __fadd2_rn(c, nm1);
+          const float2 o = __fmul2_rn(r2, __ffma2_rn(make_float2(h[e], h[e + 1]), nm2, c));
+          g[e] = o.x;
+          g[e + 1] = o.y;
         }
         st_stream(orow + vi, Vec<T>::pack(g));
       }
@@ -581,7 +592,11 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
     const int64_t nv = cols / Traits<T>::kVec;
     const bool ok16 = cols % Traits<T>::kVec == 0 && (uintptr_t)dy % 16 == 0 && (uintptr_t)y % 16 == 0 &&
                       (uintptr_t)dx % 16 == 0;
+#ifdef LMBP_NORM_NO_TMA
+    const bool want = ok16 && !p.vec && nv < (1 << 26);
+#else
     const bool want = ok16 && (!p.vec || nv * 32 >= 8192) && nv < (1 << 26);
+#endif
     const TmaPlan tp = want ? plan_tma((int)nv, false) : TmaPlan{false, 0, 0, 0};
     if (tp.ok) {
       launch_norm_tma<T, NORM, false>(tp, dy, y, rstd, dx, nullptr, rows, (int)nv, cols, 0.0f, s);
