@@ -15,7 +15,7 @@
 //     bytes per warp store.  16-bit types compute codes with packed x2
 //     compares (HSET2) and a bit-interleave trick, no per-element shifts.
 //   * GELU is evaluated branch-free as max(x,0) - |x| e^{-x^2/2} G(|x|),
-//     G(u) = Phi(-u) e^{u^2/2} ~= t P7(t), t = 1/(1 + k u): 2 MUFU + ~16 FMA-pipe
+//     G(u) = Phi(-u) e^{u^2/2} ~= t P6(t), t = 1/(1 + k u): 2 MUFU + ~12 FMA-pipe
 //     ops per element; SiLU as max(x,0) - u e^{-u} / (1 + e^{-u}) with the
 //     exponential split e^{-u} = (e^{-u/2})^2 so products underflow gradually.
 //     fp32 outputs add an exact split of the exponent argument ("precise").
