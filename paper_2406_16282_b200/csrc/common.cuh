@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 #include "constants.cuh"
@@ -164,6 +165,22 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
 
 // Device attribute helpers (host side).
 int sm_count();
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device,
+// once per (kernel instantiation, device).  Function attributes are per
+// device, so a process driving several GPUs sets it on each.  `mask` is the
+// caller's per-instantiation bitmask (devices 0..63); racing threads at worst
+// set the same attribute twice.
+template <typename K>
+inline cudaError_t ensure_dyn_smem(K kernel, size_t bytes, std::atomic<unsigned long long> &mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 }  // namespace lmbp
 

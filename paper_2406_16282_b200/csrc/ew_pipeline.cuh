@@ -199,18 +199,13 @@ template <class Op>
 cudaError_t launch_ew(const EwParams &p, cudaStream_t stream) {
   using Sh = EwShape<Op>;
   auto kern = ew_tma<Op>;
-  static const int occ = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::kSmem);
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, Sh::kThreads, Sh::kSmem) != cudaSuccess || b < 1)
-      b = 1;
-    return b;
-  }();
+  static std::atomic<unsigned long long> smem_set{0};
+  const cudaError_t e = ensure_dyn_smem(kern, Sh::kSmem, smem_set);
+  if (e != cudaSuccess) return e;
   const int64_t items = p.nvec / Sh::kTile + 1;
   const int64_t units = (items + LMBP_EW_UNIT - 1) / LMBP_EW_UNIT;
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
   const int grid = (int)units;  // CTAs beyond the resident ones are taken over via CLC
-  (void)occ;
   kern<<<grid, Sh::kThreads, Sh::kSmem, stream>>>(p);
   return cudaGetLastError();
 }

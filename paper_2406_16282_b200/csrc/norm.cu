@@ -26,6 +26,13 @@
 
 namespace lmbp {
 
+#ifndef LMBP_ROW_PREFETCH
+#define LMBP_ROW_PREFETCH 0
+#endif
+#ifndef LMBP_WARP_VMAX
+#define LMBP_WARP_VMAX 4
+#endif
+
 template <bool kWarpTeam>
 __device__ __forceinline__ float team_sum(float v, float *buf) {
   v = warp_sum(v);
@@ -74,16 +81,26 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
-    const uint4 *xr = x + row * nvec;
-    uint4 raw[V];
+  // Warp teams walk several rows each: the next row's loads are issued
+  // before the current row is reduced (register double buffering).
+  constexpr bool kPrefetch = kWarpTeam && LMBP_ROW_PREFETCH;
+  const int64_t stride = (int64_t)gridDim.x * teams;
+  int64_t row = (int64_t)blockIdx.x * teams + team_id;
+  uint4 raw[V];
+  auto load_row = [&](int64_t r, uint4 *dst) {
+    const uint4 *xr = x + r * nvec;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int vi = j * team + tid;
-      if (vi < nvec) raw[j] = ld_stream(xr + vi);
-      else raw[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (r < rows && vi < nvec) dst[j] = ld_stream(xr + vi);
+      else dst[j] = make_uint4(0u, 0u, 0u, 0u);
     }
+  };
+  load_row(row, raw);
+  int it = 0;
+  for (; row < rows; row += stride, ++it) {
+    uint4 nraw[V];
+    if constexpr (kPrefetch) load_row(row + stride, nraw);
     float mean = 0.0f;
     float ss = 0.0f;
     if constexpr (NORM == kNormLN) {
@@ -133,6 +150,12 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
       }
     }
     if (tid == 0) rstd[row] = r;
+    if constexpr (kPrefetch) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) raw[j] = nraw[j];
+    } else {
+      load_row(row + stride, raw);
+    }
   }
 }
 
@@ -150,23 +173,31 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
-    const uint4 *gr = dy + row * nvec;
-    const uint4 *yr = y + row * nvec;
-    const float r = rstd[row];
-    uint4 rg[V], ry[V];
+  constexpr bool kPrefetch = kWarpTeam && LMBP_ROW_PREFETCH;
+  const int64_t stride = (int64_t)gridDim.x * teams;
+  int64_t row = (int64_t)blockIdx.x * teams + team_id;
+  uint4 rg[V], ry[V];
+  auto load_row = [&](int64_t rr, uint4 *dg, uint4 *dyv) {
+    const uint4 *gr = dy + rr * nvec;
+    const uint4 *yr = y + rr * nvec;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int vi = j * team + tid;
-      if (vi < nvec) {
-        rg[j] = ld_stream(gr + vi);
-        ry[j] = ld_stream(yr + vi);
+      if (rr < rows && vi < nvec) {
+        dg[j] = ld_stream(gr + vi);
+        dyv[j] = ld_stream(yr + vi);
       } else {
-        rg[j] = make_uint4(0u, 0u, 0u, 0u);
-        ry[j] = make_uint4(0u, 0u, 0u, 0u);
+        dg[j] = make_uint4(0u, 0u, 0u, 0u);
+        dyv[j] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
+  };
+  load_row(row, rg, ry);
+  int it = 0;
+  for (; row < rows; row += stride, ++it) {
+    const float r = rstd[row];
+    uint4 ng[V], ny[V];
+    if constexpr (kPrefetch) load_row(row + stride, ng, ny);
     float2 acc = make_float2(0.0f, 0.0f);  // (sum dy, sum dy*y)
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -197,6 +228,15 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
         }
         st_stream(dr + vi, Vec<T>::pack(g));
       }
+    }
+    if constexpr (kPrefetch) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        rg[j] = ng[j];
+        ry[j] = ny[j];
+      }
+    } else {
+      load_row(row + stride, rg, ry);
     }
   }
 }
@@ -372,14 +412,12 @@ static TmaPlan plan_tma(int nvec, bool fwd) {
 }
 
 template <typename T, int NORM, bool kFwd>
-static void launch_norm_tma(const TmaPlan &tp, const void *a, const void *b, const float *rstd_in, void *out,
+static cudaError_t launch_norm_tma(const TmaPlan &tp, const void *a, const void *b, const float *rstd_in, void *out,
                             float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps, cudaStream_t s) {
   auto kern = norm_tma<T, NORM, kFwd>;
-  static int configured = 0;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = 1;
-  }
+  static std::atomic<unsigned long long> smem_set{0};
+  const cudaError_t e = ensure_dyn_smem(kern, 227 * 1024, smem_set);
+  if (e != cudaSuccess) return e;
   const int threads = tp.warps * 32;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, tp.smem) != cudaSuccess || occ < 1) occ = 1;
@@ -393,6 +431,7 @@ static void launch_norm_tma(const TmaPlan &tp, const void *a, const void *b, con
   kern<<<grid, threads, tp.smem, s>>>(reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), rstd_in,
                                       reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec, (int)cols, eps, tp.stages,
                                       rpw);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -478,7 +517,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
   const int64_t nvec = cols / kVec;
   if (nvec > 8 * 512) return p;
   p.nvec = (int)nvec;
-  if (nvec <= 4 * 32) {  // one warp per row, up to 4 vectors per lane
+  if (nvec <= LMBP_WARP_VMAX * 32) {  // one warp per row
     p.warp_team = true;
     p.team = 32;
     p.V = (int)((nvec + 31) / 32);
@@ -489,7 +528,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
     p.team = (int)team;
     p.V = (int)((nvec + team - 1) / team);
   }
-  p.vec = p.V >= 1 && p.V <= (p.warp_team ? 4 : 8);
+  p.vec = p.V >= 1 && p.V <= (p.warp_team ? LMBP_WARP_VMAX : 8);
   return p;
 }
 
@@ -497,12 +536,15 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
 // and block size (a benign race: every writer stores the same value).
 template <typename K>
 static int occupancy_of(K kernel, int threads) {
-  static int cache[33] = {0};
+  static std::atomic<int> cache[33];  // zero-initialised (static storage)
   const int slot = threads >> 5;
-  if (slot < 33 && cache[slot] > 0) return cache[slot];
+  if (slot < 33) {
+    const int c = cache[slot].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
   int b = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
-  if (slot < 33) cache[slot] = b;
+  if (slot < 33) cache[slot].store(b, std::memory_order_relaxed);
   return b;
 }
 
@@ -551,8 +593,7 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
     const bool ok16 = cols % Traits<T>::kVec == 0 && (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
     const TmaPlan tp = ok16 && nv < (1 << 26) ? plan_tma((int)nv, true) : TmaPlan{false, 0, 0, 0};
     if (tp.ok) {
-      launch_norm_tma<T, NORM, true>(tp, x, nullptr, nullptr, y, rstd, rows, (int)nv, cols, eps, s);
-      return cudaGetLastError();
+      return launch_norm_tma<T, NORM, true>(tp, x, nullptr, nullptr, y, rstd, rows, (int)nv, cols, eps, s);
     }
   }
   if (!p.vec) {
@@ -563,9 +604,9 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
   }
 #define LMBP_FWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= 4) {                                                                \
+    if constexpr (VV <= LMBP_WARP_VMAX) {                                                   \
       if (p.warp_team) {                                                                    \
-        fwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, x, y, rstd, rows, cols, eps, s);        \
+        fwd_v<T, NORM, VV, true>(p, x, y, rstd, rows, cols, eps, s);                        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \
@@ -599,8 +640,7 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
 #endif
     const TmaPlan tp = want ? plan_tma((int)nv, false) : TmaPlan{false, 0, 0, 0};
     if (tp.ok) {
-      launch_norm_tma<T, NORM, false>(tp, dy, y, rstd, dx, nullptr, rows, (int)nv, cols, 0.0f, s);
-      return cudaGetLastError();
+      return launch_norm_tma<T, NORM, false>(tp, dy, y, rstd, dx, nullptr, rows, (int)nv, cols, 0.0f, s);
     }
   }
   if (!p.vec) {
@@ -611,9 +651,9 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
   }
 #define LMBP_BWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= 4) {                                                                \
+    if constexpr (VV <= LMBP_WARP_VMAX) {                                                   \
       if (p.warp_team) {                                                                    \
-        bwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, dy, y, rstd, dx, rows, cols, s);        \
+        bwd_v<T, NORM, VV, true>(p, dy, y, rstd, dx, rows, cols, s);                        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \
