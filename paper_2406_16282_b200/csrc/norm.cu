@@ -26,13 +26,6 @@
 
 namespace lmbp {
 
-#ifndef LMBP_ROW_PREFETCH
-#define LMBP_ROW_PREFETCH 0
-#endif
-#ifndef LMBP_WARP_VMAX
-#define LMBP_WARP_VMAX 4
-#endif
-
 template <bool kWarpTeam>
 __device__ __forceinline__ float team_sum(float v, float *buf) {
   v = warp_sum(v);
@@ -81,26 +74,16 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  // Warp teams walk several rows each: the next row's loads are issued
-  // before the current row is reduced (register double buffering).
-  constexpr bool kPrefetch = kWarpTeam && LMBP_ROW_PREFETCH;
-  const int64_t stride = (int64_t)gridDim.x * teams;
-  int64_t row = (int64_t)blockIdx.x * teams + team_id;
-  uint4 raw[V];
-  auto load_row = [&](int64_t r, uint4 *dst) {
-    const uint4 *xr = x + r * nvec;
+  int it = 0;
+  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+    const uint4 *xr = x + row * nvec;
+    uint4 raw[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int vi = j * team + tid;
-      if (r < rows && vi < nvec) dst[j] = ld_stream(xr + vi);
-      else dst[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (vi < nvec) raw[j] = ld_stream(xr + vi);
+      else raw[j] = make_uint4(0u, 0u, 0u, 0u);
     }
-  };
-  load_row(row, raw);
-  int it = 0;
-  for (; row < rows; row += stride, ++it) {
-    uint4 nraw[V];
-    if constexpr (kPrefetch) load_row(row + stride, nraw);
     float mean = 0.0f;
     float ss = 0.0f;
     if constexpr (NORM == kNormLN) {
@@ -150,12 +133,6 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
       }
     }
     if (tid == 0) rstd[row] = r;
-    if constexpr (kPrefetch) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) raw[j] = nraw[j];
-    } else {
-      load_row(row + stride, raw);
-    }
   }
 }
 
@@ -173,31 +150,23 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  constexpr bool kPrefetch = kWarpTeam && LMBP_ROW_PREFETCH;
-  const int64_t stride = (int64_t)gridDim.x * teams;
-  int64_t row = (int64_t)blockIdx.x * teams + team_id;
-  uint4 rg[V], ry[V];
-  auto load_row = [&](int64_t rr, uint4 *dg, uint4 *dyv) {
-    const uint4 *gr = dy + rr * nvec;
-    const uint4 *yr = y + rr * nvec;
+  int it = 0;
+  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+    const uint4 *gr = dy + row * nvec;
+    const uint4 *yr = y + row * nvec;
+    const float r = rstd[row];
+    uint4 rg[V], ry[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int vi = j * team + tid;
-      if (rr < rows && vi < nvec) {
-        dg[j] = ld_stream(gr + vi);
-        dyv[j] = ld_stream(yr + vi);
+      if (vi < nvec) {
+        rg[j] = ld_stream(gr + vi);
+        ry[j] = ld_stream(yr + vi);
       } else {
-        dg[j] = make_uint4(0u, 0u, 0u, 0u);
-        dyv[j] = make_uint4(0u, 0u, 0u, 0u);
+        rg[j] = make_uint4(0u, 0u, 0u, 0u);
+        ry[j] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
-  };
-  load_row(row, rg, ry);
-  int it = 0;
-  for (; row < rows; row += stride, ++it) {
-    const float r = rstd[row];
-    uint4 ng[V], ny[V];
-    if constexpr (kPrefetch) load_row(row + stride, ng, ny);
     float2 acc = make_float2(0.0f, 0.0f);  // (sum dy, sum dy*y)
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -228,15 +197,6 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
         }
         st_stream(dr + vi, Vec<T>::pack(g));
       }
-    }
-    if constexpr (kPrefetch) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        rg[j] = ng[j];
-        ry[j] = ny[j];
-      }
-    } else {
-      load_row(row + stride, rg, ry);
     }
   }
 }
@@ -517,7 +477,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
   const int64_t nvec = cols / kVec;
   if (nvec > 8 * 512) return p;
   p.nvec = (int)nvec;
-  if (nvec <= LMBP_WARP_VMAX * 32) {  // one warp per row
+  if (nvec <= 4 * 32) {  // one warp per row, up to 4 vectors per lane
     p.warp_team = true;
     p.team = 32;
     p.V = (int)((nvec + 31) / 32);
@@ -528,7 +488,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
     p.team = (int)team;
     p.V = (int)((nvec + team - 1) / team);
   }
-  p.vec = p.V >= 1 && p.V <= (p.warp_team ? LMBP_WARP_VMAX : 8);
+  p.vec = p.V >= 1 && p.V <= (p.warp_team ? 4 : 8);
   return p;
 }
 
@@ -604,9 +564,9 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
   }
 #define LMBP_FWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= LMBP_WARP_VMAX) {                                                   \
+    if constexpr (VV <= 4) {                                                                \
       if (p.warp_team) {                                                                    \
-        fwd_v<T, NORM, VV, true>(p, x, y, rstd, rows, cols, eps, s);                        \
+        fwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, x, y, rstd, rows, cols, eps, s);        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \
@@ -651,9 +611,9 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
   }
 #define LMBP_BWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= LMBP_WARP_VMAX) {                                                   \
+    if constexpr (VV <= 4) {                                                                \
       if (p.warp_team) {                                                                    \
-        bwd_v<T, NORM, VV, true>(p, dy, y, rstd, dx, rows, cols, s);                        \
+        bwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, dy, y, rstd, dx, rows, cols, s);        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \

@@ -1,0 +1,46 @@
+"""Guards on the compiled kernels' resources (ptxas -v logs written by the
+build): the pipelined kernels' register counts decide how many CTAs fit per
+SM, and a silent jump (e.g. a changed __launch_bounds__) cost 9 % before.
+Skipped when the build logs are absent."""
+import os
+import re
+import subprocess
+
+import pytest
+
+OBJ = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2406_16282_b200", "_obj")
+
+
+def regs(log):
+    out = {}
+    text = open(os.path.join(OBJ, log)).read()
+    for m in re.finditer(r"Compiling entry function '([^']+)'.*?Used (\d+) registers", text, re.S):
+        out[m.group(1)] = int(m.group(2))
+    return out
+
+
+def demangle(names):
+    r = subprocess.run(["c++filt"], input="\n".join(names), capture_output=True, text=True)
+    return dict(zip(names, r.stdout.splitlines()))
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "act.ptxas.log")), reason="no build logs")
+def test_pipeline_register_budgets():
+    r = regs("act.ptxas.log")
+    d = demangle(list(r))
+    by = {d[k]: v for k, v in r.items()}
+    fwd = [v for k, v in by.items() if "ActFwdOp<__nv_bfloat16" in k]
+    bwd = [v for k, v in by.items() if "ActBwdOp<__nv_bfloat16" in k]
+    assert fwd and bwd
+    # forward CTA = 17 warps (544 threads): 2 CTAs / SM need <= 60 registers
+    assert max(fwd) <= 60, by
+    # backward CTA = 13 warps (416 threads): 2 CTAs / SM need <= 78 registers
+    assert max(bwd) <= 78, by
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "norm.ptxas.log")), reason="no build logs")
+def test_no_spills_in_hot_kernels():
+    for log in ("act.ptxas.log", "swiglu.ptxas.log"):
+        text = open(os.path.join(OBJ, log)).read()
+        spills = [int(x) for x in re.findall(r"(\d+) bytes spill stores", text)]
+        assert max(spills) == 0, log

@@ -43,7 +43,10 @@ def main():
     libs = {}
     for v in a.variants:
         name, _, defs = v.partition(":")
-        libs[name] = B.build_variant(name, [d for d in defs.split(",") if d])
+        if defs.startswith("@"):          # a prebuilt library, e.g. from another commit
+            libs[name] = os.path.join(ROOT, defs[1:])
+        else:
+            libs[name] = B.build_variant(name, [d for d in defs.split(",") if d])
     if a.build_only:
         return
     cfg = synth.CONFIGS[a.config]
