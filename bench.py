@@ -295,6 +295,41 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
             "gpu_launches": 2 * iters}
 
 
+def stepact_section(P, cfg, x, dy, stream, flush, sink, iters=20):
+    """the table-driven k-bit step activation on the
+    config's activation tensor -- k = 2 with the paper's table (bitwise equal
+    to the specialised kernel) and k = 4 -- GB/s of fwd + bwd."""
+    from paper_2406_16282_b200 import tables
+    tab = tables.REGELU2 if cfg["act"] == "gelu" else tables.RESILU2
+    b, n = x.element_size(), x.numel()
+    y, dx = torch.empty_like(x), torch.empty_like(dy)
+    out = {}
+    for k, thr, lv in ((2, tab["c"], tables.levels(tab)),
+                       (4, [-3.0 + 0.4 * i for i in range(15)], [i / 15 for i in range(16)])):
+        codes = torch.empty(P.codes_bytes_k(n, k), dtype=torch.uint8, device=x.device)
+        fns = (lambda: P.stepact_fwd(x, tab["act"], k, thr, y=y, codes=codes, stream=stream),
+               lambda: P.stepact_bwd(dy, codes, k, lv, dx=dx, stream=stream))
+        ts = []
+        for fn in fns:
+            for _ in range(3):
+                fn()
+            evs = []
+            for _ in range(iters):
+                sink.copy_(flush.sum())
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            ts.append(sum(a.elapsed_time(c) for a, c in evs) / iters * 1e3)
+        nbytes = 2 * (2 * b * n + P.codes_bytes_k(n, k))
+        out[f"k{k}"] = {"fwd_us": round(ts[0], 2), "bwd_us": round(ts[1], 2),
+                        "GB/s": round(nbytes / (ts[0] + ts[1]) / 1e3, 1),
+                        "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / 6536.0, 4)}
+    return out
+
+
 def block_section(cfg, R, dev):
     """activation bytes an FFN half-block keeps for
     backward (measured with saved_tensors_hooks, storage-deduplicated,
@@ -505,6 +540,7 @@ def main():
 
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
     block = block_section(cfg, R, dev) if rank == 0 else None
+    step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -530,6 +566,7 @@ def main():
             "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
             "reswiglu2": swiglu,
             "activation_bytes_saved_per_block": block,
+            "stepact": step_k,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -351,8 +351,13 @@ struct TmaPlan {
   size_t smem;
 };
 
-// Shared-memory budget per CTA for the ring (B200: 227 KB opt-in per CTA).
-constexpr size_t kNormSmemBudget = 200 * 1024;
+// Shared-memory budget per CTA for the ring (B200: 227 KB opt-in per CTA,
+// minus the barriers).  More rings per SM = finer row granularity: at C4
+// (16 KB row pairs) 7 rings of 2 stages would fit in 224 KB; measured no gain.
+#ifndef LMBP_NORM_SMEM_KB
+#define LMBP_NORM_SMEM_KB 200
+#endif
+constexpr size_t kNormSmemBudget = LMBP_NORM_SMEM_KB * 1024;
 
 static TmaPlan plan_tma(int nvec, bool fwd) {
   const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
