@@ -6,19 +6,17 @@
 //   backward: dx = dy * s[code], s = (0, a1, a1 + a2, 1) -- the derivative of
 //             the ReLU combination of Eq. 14.
 //
-// B200 design (DESIGN.md "Activation kernels"):
-//   * HBM-bound streaming: 16-byte vector loads/stores, lane-interleaved so
-//     every warp instruction touches 512 contiguous bytes; U vectors per thread
-//     in flight; grid = SMs x resident CTAs, grid-stride over tiles.
-//   * codes: one 16-bit word per 8 bf16/fp16 elements (one byte per 4 fp32),
-//     stored by the lane that owns the 16-byte vector -> 64 (32) contiguous
-//     bytes per warp store.  16-bit types compute codes with packed x2
-//     compares (HSET2) and a bit-interleave trick, no per-element shifts.
-//   * GELU is evaluated branch-free as max(x,0) - |x| e^{-x^2/2} G(|x|),
-//     G(u) = Phi(-u) e^{u^2/2} ~= t P6(t), t = 1/(1 + k u): 2 MUFU + ~12 FMA-pipe
-//     ops per element; SiLU as max(x,0) - u e^{-u} / (1 + e^{-u}) with the
-//     exponential split e^{-u} = (e^{-u/2})^2 so products underflow gradually.
-//     fp32 outputs add an exact split of the exponent argument ("precise").
+// B200 design (DESIGN.md 5.1):
+//   * TMA bulk-copy pipeline with cluster-launch-control work stealing
+//     (ew_pipeline.cuh): 16 KB (fwd) / 24 KB (bwd) tiles staged in shared
+//     memory by a producer warp, consumer warps compute and store with
+//     coalesced 16-byte stores; codes staged per warp and written as 16-byte
+//     vectors.  Fallbacks: a register-pipelined vector kernel (backward with a
+//     codes pointer not 16-byte aligned) and a scalar kernel (misaligned).
+//   * 16-bit types compute codes with packed x2 compares (HSET2) and a
+//     bit-interleave trick, no per-element shifts.
+//   * Element math in act_math.cuh (branch-free GELU via the Mills ratio,
+//     SiLU with e^{-u} = (e^{-u/2})^2; packed FFMA2/FMUL2).
 #include <type_traits>
 
 #include "common.cuh"
@@ -146,7 +144,7 @@ __device__ __forceinline__ uint32_t act_vec_op(const uint4 &v, uint32_t c_in, ui
     uint32_t c;
     if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
     else c = codes_vec_16<T, A>(v);
-#ifndef LMBP_DIAG_NO_MATH
+#ifndef LMBP_DIAG_NO_MATH  // diagnostic build knob (tools/sweep.py): time the pipeline without the math
 #pragma unroll
     for (int k = 0; k < kVec; k += 2) {
       const float2 r = act2_f<A, kPrecise>(make_float2(f[k], f[k + 1]));

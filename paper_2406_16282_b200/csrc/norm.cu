@@ -10,14 +10,18 @@
 // The affine is merged into the next linear layer, so there are
 // no parameter reads and no dgamma/dbeta column reductions.
 //
-// B200 design: a row is owned by a team of
-// `team` threads (one warp, or one CTA of up to 512 threads); each thread
-// holds V <= 8 lane-interleaved 16-byte vectors of the row in registers, so
-// every byte is read from HBM exactly once (two-pass statistics come from
-// registers).  Reductions: warp shuffles, then (CTA teams) one fixed-order
-// pass over per-warp partials in shared memory -> deterministic.  Persistent
-// grid-stride over rows.  Rows that are misaligned or longer than 8 x 1024
-// vectors (32768 bf16 / 16384 fp32 elements) take a scalar multi-pass path.
+// B200 design:
+//   * register teams: a row is owned by one warp (8 rows per 256-thread CTA,
+//     persistent grid) or one CTA of <= 512 threads (one CTA per row, the
+//     hardware block scheduler balances the SMs); each thread holds V <= 8
+//     lane-interleaved 16-byte vectors, so every byte is read from HBM once
+//     and the two-pass statistics come from registers.  Reductions: warp
+//     shuffles, then one fixed-order pass over per-warp partials in shared
+//     memory -> deterministic.
+//   * per-warp TMA ring (backward rows >= 8 KB, and rows too long for
+//     registers): each warp streams its rows through 2-4 shared-memory stages
+//     with cp.async.bulk on mbarriers and reduces from shared memory.
+//   * misaligned rows, or rows too long for both, take a scalar multi-pass path.
 #include <algorithm>
 #include <type_traits>
 
