@@ -290,8 +290,6 @@ def sample_rows(R, k=48, seed=0):
 def test_full_size_sampled(cfg):
     c = synth.CONFIGS[cfg]
     R, F, H, dtype = c["R"], c["F"], c["H"], c["dtype"]
-    if cfg == "c5":
-        R = R // 8                          # the per-GPU shard at N = 8 (rows 0..R/8)
     fwd, bwd = ACT[c["act"]]
     nf, nb, of, ob = NORM[c["norm"]]
     x = synth.act_input(R, F, dtype, device=DEV)
