@@ -349,6 +349,258 @@ __global__ void __launch_bounds__(512) norm_tma(const uint4 *a, const uint4 *b, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row pipeline: TMA staging + cluster-launch-control row stealing
+// (rows of >= 256 vectors, i.e. the LLaMA shapes).
+//
+// One producer warp streams whole rows (x; or dy and y) into a ring of S
+// shared-memory stages with cp.async.bulk; W consumer warps split each row
+// (V lane-interleaved 16-byte vectors per thread, kept in registers), release
+// the stage at once, reduce across the W warps through shared memory and one
+// named barrier per reduction (the producer warp never joins it), and store.
+// The grid has one CTA per row; the producer asks the hardware for
+// not-yet-started CTAs (clusterlaunchcontrol.try_cancel) and takes over their
+// rows, so rows are balanced dynamically over the SMs while each CTA keeps a
+// single pipeline.  The row a stage holds is passed in a per-stage slot.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <typename T, int NORM, bool kFwd, int V>
+__global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 *b, const float *rstd_in, uint4 *out,
+                                                    float *rstd_out, int64_t rows, int nvec, int cols, float eps,
+                                                    int stages) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kVec = Traits<T>::kVec;
+  constexpr int NIN = kFwd ? 1 : 2;
+  const int W = (int)(blockDim.x >> 5) - 1;  // consumer warps
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t row_bytes = (size_t)nvec * 16;
+  const size_t stage_bytes = row_bytes * NIN;
+  // layout: stages | clc response (16 B) | full[S] empty[S] clc_bar | slot[S] | red
+  uint4 *clc_resp = reinterpret_cast<uint4 *>(smem + (size_t)stages * stage_bytes);  // 16-byte aligned
+  uint64_t *full = reinterpret_cast<uint64_t *>(clc_resp + 1);
+  uint64_t *empty = full + stages;
+  uint64_t *clc_bar = empty + stages;
+  int64_t *slot = reinterpret_cast<int64_t *>(clc_bar + 1);
+  float2 *red = reinterpret_cast<float2 *>(slot + stages);     // [2 parities][2 reductions][16 warps]
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W);
+    }
+    mbar_init(clc_bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == W) {  // producer
+    if (lane == 0) {
+      int64_t row = blockIdx.x;
+      uint32_t ph = 0;
+      int k = 0;
+      for (;; ++k) {
+        mbar_arrive_expect_tx(clc_bar, 16);
+        clc_try_cancel(clc_resp, clc_bar);
+        const int s = k % stages;
+        mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
+        slot[s] = row;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+        uint8_t *st = smem + (size_t)s * stage_bytes;
+        bulk_g2s(st, a + row * nvec, (uint32_t)row_bytes, &full[s]);
+        if constexpr (!kFwd) bulk_g2s(st + row_bytes, b + row * nvec, (uint32_t)row_bytes, &full[s]);
+        mbar_wait(clc_bar, ph);
+        ph ^= 1u;
+        const int next = clc_query(clc_resp);
+        if (next < 0) break;
+        row = next;
+      }
+      ++k;
+      const int s = k % stages;
+      mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
+      slot[s] = -1;
+      mbar_arrive(&full[s]);
+    }
+    return;
+  }
+
+  const int nthreads = W * 32;
+  const int tid = threadIdx.x;
+  const float fcols = (float)cols;
+  for (int k = 0;; ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)(k / stages) & 1u);
+    const int64_t row = slot[s];
+    if (row < 0) break;
+    const uint8_t *st = smem + (size_t)s * stage_bytes;
+    uint4 ra[V], rb[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int vi = j * nthreads + tid;
+      if (vi < nvec) {
+        ra[j] = lds128(st + (size_t)vi * 16);
+        if constexpr (!kFwd) rb[j] = lds128(st + row_bytes + (size_t)vi * 16);
+      } else {
+        ra[j] = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (!kFwd) rb[j] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // row is in registers: the stage may be refilled
+    float2 *rk = red + (k & 1) * 32;
+    uint4 *orow = out + row * nvec;
+    if constexpr (kFwd) {
+      float mean = 0.0f;
+      if constexpr (NORM == kNormLN) {
+        float sm = 0.0f;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          float f[kVec];
+          Vec<T>::unpack(ra[j], f);
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) sm += f[e];
+        }
+        sm = warp_sum(sm);
+        if (lane == 0) rk[warp].x = sm;
+        consumer_bar(nthreads);
+        float t = 0.0f;
+        for (int w = 0; w < W; ++w) t += rk[w].x;
+        mean = __fdiv_rn(t, fcols);
+      }
+      float ss = 0.0f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (j * nthreads + tid < nvec) {
+          float f[kVec];
+          Vec<T>::unpack(ra[j], f);
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const float d = NORM == kNormLN ? __fsub_rn(f[e], mean) : f[e];
+            ss = fmaf(d, d, ss);
+          }
+        }
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) rk[16 + warp].x = ss;
+      consumer_bar(nthreads);
+      float t = 0.0f;
+      for (int w = 0; w < W; ++w) t += rk[16 + w].x;
+      const float r = rsqrtf(__fadd_rn(__fdiv_rn(t, fcols), eps));
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int vi = j * nthreads + tid;
+        if (vi < nvec) {
+          float f[kVec];
+          Vec<T>::unpack(ra[j], f);
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) f[e] = __fmul_rn(NORM == kNormLN ? __fsub_rn(f[e], mean) : f[e], r);
+          st_stream(orow + vi, Vec<T>::pack(f));
+        }
+      }
+      if (tid == 0) rstd_out[row] = r;
+    } else {
+      const float r = rstd_in[row];
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        float g[kVec], h[kVec];
+        Vec<T>::unpack(ra[j], g);
+        Vec<T>::unpack(rb[j], h);
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          if constexpr (NORM == kNormLN) acc.x += g[e];
+          acc.y = fmaf(g[e], h[e], acc.y);
+        }
+      }
+      acc = warp_sum2(acc);
+      if (lane == 0) rk[warp] = acc;
+      consumer_bar(nthreads);
+      float2 t = make_float2(0.0f, 0.0f);
+      for (int w = 0; w < W; ++w) {
+        t.x += rk[w].x;
+        t.y += rk[w].y;
+      }
+      const float m1 = NORM == kNormLN ? __fdiv_rn(t.x, fcols) : 0.0f;
+      const float m2 = __fdiv_rn(t.y, fcols);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int vi = j * nthreads + tid;
+        if (vi < nvec) {
+          float g[kVec], h[kVec];
+          Vec<T>::unpack(ra[j], g);
+          Vec<T>::unpack(rb[j], h);
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const float c = NORM == kNormLN ? __fsub_rn(g[e], m1) : g[e];
+            g[e] = __fmul_rn(r, fmaf(-h[e], m2, c));
+          }
+          st_stream(orow + vi, Vec<T>::pack(g));
+        }
+      }
+    }
+  }
+}
+
+struct RowTmaPlan {
+  bool ok;
+  int warps;   // consumer warps
+  int V;       // vectors per thread
+  int stages;
+  size_t smem;
+};
+
+static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
+  RowTmaPlan p{false, 0, 0, 0, 0};
+  if (nvec < 256 || nvec > 16 * 32 * 8) return p;
+  int warps = (int)((nvec + 4 * 32 - 1) / (4 * 32));  // aim for 4 vectors per thread
+  if (warps > 16) warps = 16;
+  const int V = (int)((nvec + warps * 32 - 1) / (warps * 32));
+  if (V > 8) return p;
+  const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
+  int stages = (int)std::min<size_t>(4, (size_t)(96 * 1024) / stage);
+  if (stages < 2) stages = 2;
+  const size_t tail = 16 + (2 * (size_t)stages + 1) * 8 + (size_t)stages * 8 + 64 * sizeof(float2);
+  p.smem = (size_t)stages * stage + tail;
+  if (p.smem > 227 * 1024) return p;
+  p.ok = true;
+  p.warps = warps;
+  p.V = V;
+  p.stages = stages;
+  return p;
+}
+
+template <typename T, int NORM, bool kFwd, int V>
+static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const void *b, const float *rstd_in,
+                                    void *out, float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps,
+                                    cudaStream_t s) {
+  auto kern = norm_row_tma<T, NORM, kFwd, V>;
+  static std::atomic<unsigned long long> smem_set{0};
+  const cudaError_t e = ensure_dyn_smem(kern, 227 * 1024, smem_set);
+  if (e != cudaSuccess) return e;
+  if (rows > 0x7fffffff) return cudaErrorInvalidValue;
+  kern<<<(int)rows, (rp.warps + 1) * 32, rp.smem, s>>>(reinterpret_cast<const uint4 *>(a),
+                                                        reinterpret_cast<const uint4 *>(b), rstd_in,
+                                                        reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec,
+                                                        (int)cols, eps, rp.stages);
+  return cudaGetLastError();
+}
+
+template <typename T, int NORM, bool kFwd>
+static cudaError_t launch_row_tma(const RowTmaPlan &rp, const void *a, const void *b, const float *rstd_in, void *out,
+                                  float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps, cudaStream_t s) {
+  switch (rp.V) {
+    case 1: return launch_row_tma_v<T, NORM, kFwd, 1>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 2: return launch_row_tma_v<T, NORM, kFwd, 2>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 3: return launch_row_tma_v<T, NORM, kFwd, 3>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 4: return launch_row_tma_v<T, NORM, kFwd, 4>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 5: return launch_row_tma_v<T, NORM, kFwd, 5>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 6: return launch_row_tma_v<T, NORM, kFwd, 6>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 7: return launch_row_tma_v<T, NORM, kFwd, 7>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    default: return launch_row_tma_v<T, NORM, kFwd, 8>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+  }
+}
+
 struct TmaPlan {
   bool ok;
   int warps, stages;
@@ -554,6 +806,12 @@ template <typename T, int NORM>
 static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
                               cudaStream_t s) {
   const RowPlan p = plan_rows<T>(cols, x, y, y);
+#ifdef LMBP_ROW_TMA_FWD  // measured slower than the register teams for the forward (C4 24.6 vs 20.5 us)
+  if (p.vec && rows > 0) {
+    const RowTmaPlan rp = plan_row_tma(p.nvec, true);
+    if (rp.ok) return launch_row_tma<T, NORM, true>(rp, x, nullptr, nullptr, y, rstd, rows, p.nvec, cols, eps, s);
+  }
+#endif
   // Forward: the register-resident team kernel measured faster than the TMA
   // ring at every BASELINE shape (C4 21.9 vs 23.5 us, C5 104 vs 117 us), so
   // the ring is only used where registers cannot hold a row.
@@ -594,6 +852,12 @@ template <typename T, int NORM>
 static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
                               int64_t cols, cudaStream_t s) {
   const RowPlan p = plan_rows<T>(cols, dy, y, dx);
+#ifndef LMBP_NO_ROW_TMA  // backward rows >= 256 vectors: row pipeline (C5 160 -> 147 us; C4 equal)
+  if (p.vec && rows > 0) {
+    const RowTmaPlan rp = plan_row_tma(p.nvec, false);
+    if (rp.ok) return launch_row_tma<T, NORM, false>(rp, dy, y, rstd, dx, nullptr, rows, p.nvec, cols, 0.0f, s);
+  }
+#endif
   // Backward: the TMA ring wins once a row pair (dy, y) is >= 8 KB (C4: 32.8
   // vs 34.6 us, C5: 160 vs 172 us); short rows (H = 768) stay on the register
   // team kernel (C2/C3 measured faster there).  Rows too long for registers
