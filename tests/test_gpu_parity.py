@@ -341,3 +341,64 @@ def test_modules_autograd_and_saved_bytes():
     assert both == R * H * 2 + 4 * R + H * 64 * 2                        # y + rstd + weight
     exact = P.saved_bytes(lambda t: lin(torch.nn.functional.layer_norm(t, (H,))), xn)
     assert exact > both
+
+
+# ---------------------------------------------------------------------------
+# CUDA graphs: every entry point is capturable (no allocation, no sync, no
+# host-side state) and a replayed step is bitwise identical to eager.
+# ---------------------------------------------------------------------------
+def test_cuda_graph_capture_replay():
+    R, F, H = 256, 11008, 4096
+    x = synth.act_input(R, F, "bf16").to(DEV)
+    dy = synth.grad_input(R, F, "bf16").to(DEV)
+    xn = synth.norm_input(R, H, "bf16").to(DEV)
+    gn = synth.grad_input(R, H, "bf16").to(DEV)
+    bufs = dict(y=torch.empty_like(x), dx=torch.empty_like(x), codes=torch.empty(P.codes_bytes(R * F), dtype=torch.uint8, device=DEV),
+                yn=torch.empty_like(xn), dxn=torch.empty_like(xn), rstd=torch.empty(R, device=DEV))
+
+    def step(s):
+        P.msrms_fwd(xn, 1e-6, y=bufs["yn"], rstd=bufs["rstd"], stream=s)
+        P.resilu2_fwd(x, y=bufs["y"], codes=bufs["codes"], stream=s)
+        P.resilu2_bwd(dy, bufs["codes"], dx=bufs["dx"], stream=s)
+        P.msrms_bwd(gn, bufs["yn"], bufs["rstd"], dx=bufs["dxn"], stream=s)
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        step(s)                                   # warm-up (attributes, occupancy caches)
+    s.synchronize()
+    eager = {k: v.clone() for k, v in bufs.items()}
+    for v in bufs.values():
+        v.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step(s)
+    for v in bufs.values():
+        v.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for k in bufs:
+        assert st(bufs[k]).tobytes() == st(eager[k]).tobytes(), k
+
+
+def test_random_shapes():
+    rng = np.random.default_rng(2406)
+    for _ in range(24):
+        dtype = rng.choice(["f32", "bf16", "f16"])
+        kind = rng.choice(["gelu", "silu"])
+        R, F = int(rng.integers(1, 40)), int(rng.integers(1, 9000))
+        x = synth.act_input(R, F, dtype, mode="coverage", base=int(rng.integers(1 << 30)))
+        dy = synth.grad_input(R, F, dtype)
+        fwd, bwd = ACT[kind]
+        y, codes = fwd(x.to(DEV))
+        torch.cuda.synchronize()
+        c_ref = check_act_fwd(kind, dtype, x, y, codes)
+        dx = bwd(dy.to(DEV), torch.from_numpy(c_ref).to(DEV))
+        torch.cuda.synchronize()
+        check_act_bwd(kind, dtype, c_ref, dy, dx)
+        norm = rng.choice(["ln", "rms"])
+        H = int(rng.integers(1, 9000))
+        xn = synth.norm_input(R, H, dtype)
+        yn, r = NORM[norm][0](xn.to(DEV), 1e-6)
+        torch.cuda.synchronize()
+        check_norm_fwd(norm, dtype, xn, 1e-6, yn, r)
