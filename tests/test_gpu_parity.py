@@ -402,3 +402,21 @@ def test_random_shapes():
         yn, r = NORM[norm][0](xn.to(DEV), 1e-6)
         torch.cuda.synchronize()
         check_norm_fwd(norm, dtype, xn, 1e-6, yn, r)
+
+
+def test_more_than_2_31_elements():
+    """int64 indexing end to end: an activation tensor of 2^31 + 98304
+    elements (bf16, 4.3 GB), sampled rows checked against the oracle, codes
+    of the last rows included."""
+    R, F = (1 << 16) + 3, 32768
+    x = synth.act_input(R, F, "bf16", device=DEV)
+    dy = synth.grad_input(R, F, "bf16", device=DEV)
+    y, codes = P.resilu2_fwd(x)
+    dx = P.resilu2_bwd(dy, codes)
+    torch.cuda.synchronize()
+    rows = [0, 1, 40000, R - 2, R - 1]
+    idx = torch.tensor(rows, device=DEV)
+    c_ref = check_act_fwd("silu", "bf16", x[idx].cpu(), y[idx], codes.view(R, F // 4)[idx].reshape(-1))
+    check_act_bwd("silu", "bf16", c_ref, dy[idx].cpu(), dx[idx])
+    del x, dy, y, dx, codes
+    torch.cuda.empty_cache()

@@ -68,7 +68,7 @@ def main():
     sp = st.cuda_stream
     b = synth.ELEM_BYTES[dt]
     n = R * F
-    nbytes = {"copy": 2 * b * n, "act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
+    nbytes = {"ncopy": 2 * b * R * H, "copy": 2 * b * n, "act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
               "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R}
     act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
     nrm = "msln" if cfg["norm"] == "ln" else "msrms"
@@ -76,6 +76,7 @@ def main():
         L = load(path)
         calls = {
             "copy": lambda: (y.copy_(x), 0)[1],     # torch copy of the same tensors: same-footprint reference
+            "ncopy": lambda: (yn.copy_(xn), 0)[1],  # torch copy of the norm tensor
             "act_fwd": lambda: getattr(L, act + "_fwd")(x.data_ptr(), y.data_ptr(), codes.data_ptr(), R, F, DT[dt], sp),
             "act_bwd": lambda: getattr(L, act + "_bwd")(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), R, F, DT[dt], sp),
             "norm_fwd": lambda: getattr(L, nrm + "_fwd")(xn.data_ptr(), yn.data_ptr(), rstd.data_ptr(), R, H, 1e-6,
