@@ -135,8 +135,14 @@ __device__ __forceinline__ float2 silu2_f(float2 x) {
     const float2 eh = make_float2(ex2_approx(a.x), ex2_approx(a.y));
     const float2 d = __ffma2_rn(eh, eh, f2(1.0f));
     const float2 s = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+#ifndef LMBP_SILU_SCALAR_SUB
+    // -q directly (exact negation): max(x,0) - q as one FADD2
+    const float2 nq = __fmul2_rn(__fmul2_rn(__fmul2_rn(make_float2(-u.x, -u.y), eh), s), eh);
+    return __fadd2_rn(make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)), nq);
+#else
     const float2 q = __fmul2_rn(__fmul2_rn(__fmul2_rn(u, eh), s), eh);
     return make_float2(__fsub_rn(fmaxf(x.x, 0.0f), q.x), __fsub_rn(fmaxf(x.y, 0.0f), q.y));
+#endif
   }
 }
 
