@@ -163,6 +163,14 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
   return v;
 }
 
+// Runtime step table for the k-bit activations (stepact.cu): binary32
+// thresholds rounded toward -inf and binary32 levels, k in {1, 2, 4}.
+struct StepTable {
+  float thr[15];
+  float lvl[16];
+  int k;
+};
+
 // Device attribute helpers (host side).
 int sm_count();
 

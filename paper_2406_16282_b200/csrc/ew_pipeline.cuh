@@ -31,6 +31,7 @@ struct EwParams {
   uint8_t *codes_out;        // packed codes written by forward ops
   int64_t nvec;              // whole 16-byte vectors
   int64_t n;                 // elements
+  StepTable tab;             // runtime step table (k-bit step activations only)
 };
 
 template <class Op> struct EwShape {
@@ -50,13 +51,15 @@ template <class Op> struct EwShape {
 
 template <int kCodeOut>
 __device__ __forceinline__ void put_code(uint8_t *base, int64_t i, uint32_t c) {
-  if constexpr (kCodeOut == 2) reinterpret_cast<uint16_t *>(base)[i] = (uint16_t)c;
+  if constexpr (kCodeOut == 4) reinterpret_cast<uint32_t *>(base)[i] = c;
+  else if constexpr (kCodeOut == 2) reinterpret_cast<uint16_t *>(base)[i] = (uint16_t)c;
   else if constexpr (kCodeOut == 1) base[i] = (uint8_t)c;
 }
 
 template <int kCodeIn>
 __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
-  if constexpr (kCodeIn == 2) return reinterpret_cast<const uint16_t *>(base)[i];
+  if constexpr (kCodeIn == 4) return reinterpret_cast<const uint32_t *>(base)[i];
+  else if constexpr (kCodeIn == 2) return reinterpret_cast<const uint16_t *>(base)[i];
   else if constexpr (kCodeIn == 1) return base[i];
   else return 0u;
 }

@@ -18,13 +18,7 @@ cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, i
 cudaError_t norm_bwd(int kind, int dtype, const void *dy, const void *y, const float *rstd, void *dx,
                      int64_t rows, int64_t cols, cudaStream_t s);
 
-// Runtime step table for the k-bit activations (stepact.cu): binary32
-// thresholds rounded toward -inf and binary32 levels, k in {1, 2, 4}.
-struct StepTable {
-  float thr[15];
-  float lvl[16];
-  int k;
-};
+struct StepTable;  // common.cuh
 cudaError_t stepact_fwd(int act, int dtype, const StepTable &t, const void *x, void *y, uint8_t *codes, int64_t n,
                         cudaStream_t s);
 cudaError_t stepact_bwd(int dtype, const StepTable &t, const void *dy, const uint8_t *codes, void *dx, int64_t n,

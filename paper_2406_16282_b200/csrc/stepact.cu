@@ -14,6 +14,7 @@
 // A thread owns groups of 8 elements = k bytes of codes.
 #include "act_math.cuh"
 #include "common.cuh"
+#include "ew_pipeline.cuh"
 #include "kernels.h"
 
 namespace lmbp {
@@ -112,6 +113,95 @@ __global__ void __launch_bounds__(256) stepact_bwd_k(const T *dy, const uint8_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA/CLC pipeline path (ew_pipeline.cuh): one 16-byte vector of kVec
+// elements yields kVec k bits = kVec k / 8 whole bytes of codes (needs
+// kVec k >= 8: every case except fp32 with k = 1, which keeps the simple
+// kernel).  Same per-element arithmetic as the simple kernel -> bitwise equal.
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ float level_sel(const float *L, uint32_t c) {
+  if constexpr (K == 1) {
+    return c ? L[1] : L[0];
+  } else if constexpr (K == 2) {
+    const float lo = (c & 1u) ? L[1] : L[0];
+    const float hi = (c & 1u) ? L[3] : L[2];
+    return (c & 2u) ? hi : lo;
+  } else {
+    float a[8], b[4], d[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (c & 1u) ? L[2 * i + 1] : L[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = (c & 2u) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) d[i] = (c & 4u) ? b[2 * i + 1] : b[2 * i];
+    return (c & 8u) ? d[1] : d[0];
+  }
+}
+
+template <typename T, int A, bool kPrecise, int K>
+struct StepFwdOp {
+  static constexpr int kVecT = Traits<T>::kVec;
+  static constexpr int W = 16, U = 2, S = 4, kIn = 1, kCodeIn = 0, kCodeOut = kVecT * K / 8;
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p) {
+    float f[kVecT];
+    Vec<T>::unpack(v[0], f);
+    uint32_t w = 0;
+#pragma unroll
+    for (int e = 0; e < kVecT; ++e) w |= step_code<K>(f[e], p.tab.thr) << (K * e);
+#pragma unroll
+    for (int e = 0; e < kVecT; e += 2) {
+      const float2 r = act2_f<A, kPrecise>(make_float2(f[e], f[e + 1]));
+      f[e] = r.x;
+      f[e + 1] = r.y;
+    }
+    st_stream(p.out[0] + i, Vec<T>::pack(f));
+    return w;
+  }
+  __device__ static void tail(const EwParams &p) {
+    const int64_t j0 = p.nvec * kVecT;
+    if (j0 >= p.n) return;
+    const T *x = reinterpret_cast<const T *>(p.in[0]);
+    T *y = reinterpret_cast<T *>(p.out[0]);
+    uint32_t w = 0;
+    for (int64_t j = j0; j < p.n; ++j) {
+      const float f = to_f32<T>(x[j]);
+      w |= step_code<K>(f, p.tab.thr) << (K * (j - j0));
+      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+    }
+    const int nbytes = (int)(((p.n - j0) * K + 7) / 8);
+    for (int b = 0; b < nbytes; ++b) p.codes_out[j0 * K / 8 + b] = (uint8_t)(w >> (8 * b));
+  }
+};
+
+template <typename T, int K>
+struct StepBwdOp {
+  static constexpr int kVecT = Traits<T>::kVec;
+  static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = kVecT * K / 8, kCodeOut = 0;
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const EwParams &p) {
+    constexpr uint32_t kMask = (1u << K) - 1u;
+    float L[1 << K];
+#pragma unroll
+    for (int q = 0; q < (1 << K); ++q) L[q] = p.tab.lvl[q];
+    float f[kVecT];
+    Vec<T>::unpack(v[0], f);
+#pragma unroll
+    for (int e = 0; e < kVecT; ++e) f[e] = __fmul_rn(f[e], level_sel<K>(L, (c >> (K * e)) & kMask));
+    st_stream(p.out[0] + i, Vec<T>::pack(f));
+    return 0u;
+  }
+  __device__ static void tail(const EwParams &p) {
+    constexpr uint32_t kMask = (1u << K) - 1u;
+    const T *dy = reinterpret_cast<const T *>(p.in[0]);
+    T *dx = reinterpret_cast<T *>(p.out[0]);
+    for (int64_t j = p.nvec * kVecT; j < p.n; ++j) {
+      const int64_t bit = K * j;
+      const uint32_t c = (p.codes_in[bit >> 3] >> (bit & 7)) & kMask;
+      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), p.tab.lvl[c]));
+    }
+  }
+};
+
 static int step_grid(int64_t groups) {
   const int64_t want = (groups + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
@@ -122,6 +212,18 @@ static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t
                                  cudaStream_t s) {
   constexpr bool kPrecise = std::is_same<T, float>::value;
   const bool vec = (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
+  if constexpr (Traits<T>::kVec * K >= 8) {
+    if (vec && (uintptr_t)codes % 16 == 0) {
+      EwParams p{};
+      p.in[0] = reinterpret_cast<const uint4 *>(x);
+      p.out[0] = reinterpret_cast<uint4 *>(y);
+      p.codes_out = codes;
+      p.nvec = n / Traits<T>::kVec;
+      p.n = n;
+      p.tab = tab;
+      return launch_ew<StepFwdOp<T, A, kPrecise, K>>(p, s);
+    }
+  }
   stepact_fwd_k<T, A, kPrecise, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(x),
                                                                      reinterpret_cast<T *>(y), codes, n, tab, vec);
   return cudaGetLastError();
@@ -131,6 +233,18 @@ template <typename T, int K>
 static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx, int64_t n, const StepTable &tab,
                                  cudaStream_t s) {
   const bool vec = (uintptr_t)dy % 16 == 0 && (uintptr_t)dx % 16 == 0;
+  if constexpr (Traits<T>::kVec * K >= 8) {
+    if (vec && (uintptr_t)codes % 16 == 0) {
+      EwParams p{};
+      p.in[0] = reinterpret_cast<const uint4 *>(dy);
+      p.codes_in = codes;
+      p.out[0] = reinterpret_cast<uint4 *>(dx);
+      p.nvec = n / Traits<T>::kVec;
+      p.n = n;
+      p.tab = tab;
+      return launch_ew<StepBwdOp<T, K>>(p, s);
+    }
+  }
   stepact_bwd_k<T, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(dy), codes,
                                                         reinterpret_cast<T *>(dx), n, tab, vec);
   return cudaGetLastError();

@@ -68,3 +68,22 @@ def test_stepact_bad_tables():
         P.stepact_fwd(x, "gelu", 2, [1.0, 0.0, 2.0])           # not increasing
     with pytest.raises(RuntimeError, match="TABLE"):
         P.stepact_fwd(x, "gelu", 2, [0.0, float("nan"), 2.0])
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_stepact_paths_bitwise(k, dtype):
+    """TMA pipeline path (aligned) == simple kernel path (misaligned codes)."""
+    rng = np.random.default_rng(10 + k)
+    c, s = _tables(k, rng)
+    R, F = 33, 4099
+    x = synth.act_input(R, F, dtype, mode="coverage").to(DEV)
+    dy = synth.grad_input(R, F, dtype).to(DEV)
+    y0, c0 = P.stepact_fwd(x, "silu", k, c)
+    dx0 = P.stepact_bwd(dy, c0, k, s)
+    cb = torch.empty(c0.numel() + 1, dtype=torch.uint8, device=DEV)
+    y1, c1 = P.stepact_fwd(x, "silu", k, c, codes=cb[1:])
+    dx1 = P.stepact_bwd(dy, c1, k, s)
+    torch.cuda.synchronize()
+    assert torch.equal(c0, c1)
+    assert st(y0).tobytes() == st(y1).tobytes() and st(dx0).tobytes() == st(dx1).tobytes()
