@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <atomic>
 #include <cstdint>
+#include <type_traits>
 
 #include "constants.cuh"
 

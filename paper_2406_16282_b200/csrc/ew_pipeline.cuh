@@ -15,9 +15,10 @@
 //   static constexpr int kIn;       input streams (1..3)
 //   static constexpr int kCodeIn;   bytes of packed codes read per vector (0, 1, 2)
 //   static constexpr int kCodeOut;  // bytes of packed codes written per vector (0, 1, 2)
-//   __device__ static uint32_t apply(const uint4 (&v)[kIn], uint32_t code, int64_t i, const EwParams &p);
+//   using Params = ...;            optional, a struct derived from EwParams (default EwParams)
+//   __device__ static uint32_t apply(const uint4 (&v)[kIn], uint32_t code, int64_t i, const Params &p);
 //       -> the code word of vector i (ignored when kCodeOut == 0)
-//   __device__ static void tail(const EwParams &p);   elements [nvec * kVec, n), one thread
+//   __device__ static void tail(const Params &p);   elements [nvec * kVec, n), one thread
 #pragma once
 
 #include "common.cuh"
@@ -31,8 +32,14 @@ struct EwParams {
   uint8_t *codes_out;        // packed codes written by forward ops
   int64_t nvec;              // whole 16-byte vectors
   int64_t n;                 // elements
-  StepTable tab;             // runtime step table (k-bit step activations only)
 };
+
+// An Op may extend the parameters (`using Params = ...;`, derived from
+// EwParams); the kernel takes that type by value, so only the ops that need
+// extra data pay for a larger parameter block (a 128-byte step table in every
+// op's parameters cost the fp32 SwiGLU backward a register spill).
+template <class Op, class = void> struct ParamsOf { using type = EwParams; };
+template <class Op> struct ParamsOf<Op, std::void_t<typename Op::Params>> { using type = typename Op::Params; };
 
 template <class Op> struct EwShape {
   static constexpr int kTile = Op::W * 32 * Op::U;  // vectors per tile
@@ -78,7 +85,7 @@ __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
 #endif
 
 template <class Op>
-__global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const EwParams p) {
+__global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const typename ParamsOf<Op>::type p) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Sh = EwShape<Op>;
   constexpr int W = Op::W, U = Op::U, S = Op::S, NIN = Op::kIn, TILE = Sh::kTile;
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const EwParams p
 
 // Launch one CTA per work unit; resident CTAs steal the rest through CLC.
 template <class Op>
-cudaError_t launch_ew(const EwParams &p, cudaStream_t stream) {
+cudaError_t launch_ew(const typename ParamsOf<Op>::type &p, cudaStream_t stream) {
   using Sh = EwShape<Op>;
   auto kern = ew_tma<Op>;
   static std::atomic<unsigned long long> smem_set{0};

@@ -139,11 +139,16 @@ __device__ __forceinline__ float level_sel(const float *L, uint32_t c) {
   }
 }
 
+struct StepEwParams : EwParams {
+  StepTable tab;  // runtime step table
+};
+
 template <typename T, int A, bool kPrecise, int K>
 struct StepFwdOp {
+  using Params = StepEwParams;
   static constexpr int kVecT = Traits<T>::kVec;
   static constexpr int W = 16, U = 2, S = 4, kIn = 1, kCodeIn = 0, kCodeOut = kVecT * K / 8;
-  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p) {
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p) {
     float f[kVecT];
     Vec<T>::unpack(v[0], f);
     uint32_t w = 0;
@@ -158,7 +163,7 @@ struct StepFwdOp {
     st_stream(p.out[0] + i, Vec<T>::pack(f));
     return w;
   }
-  __device__ static void tail(const EwParams &p) {
+  __device__ static void tail(const StepEwParams &p) {
     const int64_t j0 = p.nvec * kVecT;
     if (j0 >= p.n) return;
     const T *x = reinterpret_cast<const T *>(p.in[0]);
@@ -176,9 +181,10 @@ struct StepFwdOp {
 
 template <typename T, int K>
 struct StepBwdOp {
+  using Params = StepEwParams;
   static constexpr int kVecT = Traits<T>::kVec;
   static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = kVecT * K / 8, kCodeOut = 0;
-  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const EwParams &p) {
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const StepEwParams &p) {
     constexpr uint32_t kMask = (1u << K) - 1u;
     float L[1 << K];
 #pragma unroll
@@ -190,7 +196,7 @@ struct StepBwdOp {
     st_stream(p.out[0] + i, Vec<T>::pack(f));
     return 0u;
   }
-  __device__ static void tail(const EwParams &p) {
+  __device__ static void tail(const StepEwParams &p) {
     constexpr uint32_t kMask = (1u << K) - 1u;
     const T *dy = reinterpret_cast<const T *>(p.in[0]);
     T *dx = reinterpret_cast<T *>(p.out[0]);
@@ -214,7 +220,7 @@ static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t
   const bool vec = (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
   if constexpr (Traits<T>::kVec * K >= 8) {
     if (vec && (uintptr_t)codes % 16 == 0) {
-      EwParams p{};
+      StepEwParams p{};
       p.in[0] = reinterpret_cast<const uint4 *>(x);
       p.out[0] = reinterpret_cast<uint4 *>(y);
       p.codes_out = codes;
@@ -235,7 +241,7 @@ static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx,
   const bool vec = (uintptr_t)dy % 16 == 0 && (uintptr_t)dx % 16 == 0;
   if constexpr (Traits<T>::kVec * K >= 8) {
     if (vec && (uintptr_t)codes % 16 == 0) {
-      EwParams p{};
+      StepEwParams p{};
       p.in[0] = reinterpret_cast<const uint4 *>(dy);
       p.codes_in = codes;
       p.out[0] = reinterpret_cast<uint4 *>(dx);
