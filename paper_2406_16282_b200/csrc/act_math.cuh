@@ -92,8 +92,11 @@ __device__ __forceinline__ float silu_f(float x) {
   const float u = fabsf(x);
   const float eh = exp_neg_half<kPrecise>(u);       // e^{-u/2}, never subnormal for u < 174
   const float s = rcp_approx(fmaf(eh, eh, 1.0f));   // 1 / (1 + e^{-u})
-  const float q = __fmul_rn(__fmul_rn(__fmul_rn(u, eh), s), eh);
-  return __fsub_rn(fmaxf(x, 0.0f), q);
+  // max(x,0) - (u eh s) eh with one rounding (an explicit FMA, as in the packed
+  // path: ptxas fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2 regardless of the
+  // rounding modifier, so the contract is written as the fused form on both).
+  const float nq = __fmul_rn(__fmul_rn(-u, eh), s);
+  return fmaf(nq, eh, fmaxf(x, 0.0f));
 }
 
 // Packed-pair versions on sm_100's f32x2 FMA pipe (FFMA2 / FMUL2): the same
@@ -135,14 +138,8 @@ __device__ __forceinline__ float2 silu2_f(float2 x) {
     const float2 eh = make_float2(ex2_approx(a.x), ex2_approx(a.y));
     const float2 d = __ffma2_rn(eh, eh, f2(1.0f));
     const float2 s = make_float2(rcp_approx(d.x), rcp_approx(d.y));
-#ifndef LMBP_SILU_SCALAR_SUB
-    // -q directly (exact negation): max(x,0) - q as one FADD2
-    const float2 nq = __fmul2_rn(__fmul2_rn(__fmul2_rn(make_float2(-u.x, -u.y), eh), s), eh);
-    return __fadd2_rn(make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)), nq);
-#else
-    const float2 q = __fmul2_rn(__fmul2_rn(__fmul2_rn(u, eh), s), eh);
-    return make_float2(__fsub_rn(fmaxf(x.x, 0.0f), q.x), __fsub_rn(fmaxf(x.y, 0.0f), q.y));
-#endif
+    const float2 nq = __fmul2_rn(__fmul2_rn(make_float2(-u.x, -u.y), eh), s);
+    return __ffma2_rn(nq, eh, make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
   }
 }
 
