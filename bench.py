@@ -56,6 +56,7 @@ def parse(argv=None):
     ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-fitter", action="store_true", help="skip the coefficient-fitter section")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the full config (its own batch); "
                          "strong: the config's rows are split across ranks")
@@ -295,7 +296,7 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
             "gpu_launches": 2 * iters}
 
 
-def stepact_section(P, cfg, x, dy, stream, flush, sink, iters=20):
+def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     """the table-driven k-bit step activation on the
     config's activation tensor -- k = 2 with the paper's table (bitwise equal
     to the specialised kernel) and k = 4 -- GB/s of fwd + bwd."""
@@ -326,7 +327,70 @@ def stepact_section(P, cfg, x, dy, stream, flush, sink, iters=20):
         nbytes = 2 * (2 * b * n + P.codes_bytes_k(n, k))
         out[f"k{k}"] = {"fwd_us": round(ts[0], 2), "bwd_us": round(ts[1], 2),
                         "GB/s": round(nbytes / (ts[0] + ts[1]) / 1e3, 1),
-                        "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / 6536.0, 4)}
+                        "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / peak, 4)}
+    return out
+
+
+PAPER_THETA = {  # P:L1062-1063 (GELU), P:L1139-1140 (SiLU), P:L1346-1347 (ReGELU2-d)
+    ("gelu", "h"): [-0.04922261145617846, 1.0979632065417297, -3.1858810036855245, -0.001178821281161997,
+                    3.190832613414926],
+    ("silu", "h"): [-0.04060357190528599, 1.080925428529668, -6.3050461001646445, -0.0008684942046214787,
+                    6.325815242089708],
+    ("gelu", "dh"): [0.32465931184406527, 0.34812875668739607, -0.4535743722857079, -0.0010587205574873046,
+                     0.4487575313884231],
+}
+
+
+def fitter_section(stream, cpu=True, chains=148 * 3 * 128, iters=1000, n_obj=148 * 3 * 128 * 4):
+    """the offline coefficient fitter.  (1) batched
+    objective throughput (J evaluations/s; one thread per theta, FP64-bound);
+    (2) a full simulated-annealing fit per (act, objective) of App. E / App. I
+    -- time, the J reached vs J at the paper's constants (both by the GPU
+    objective), the fitted constants; (3) the oracle's (QUADPACK) J/s on the
+    host for the cpu baseline."""
+    from paper_2406_16282_b200 import fit as gfit
+    from paper_2406_16282_b200 import ops
+    out = {"chains": chains, "iters": iters}
+    g = torch.Generator(device="cuda").manual_seed(2406)
+    for act in ("gelu", "silu"):
+        th = torch.tensor(PAPER_THETA[(act, "h")], dtype=torch.float64, device="cuda")
+        batch = (th + 0.05 * torch.randn(n_obj, 5, dtype=torch.float64, device="cuda", generator=g)).contiguous()
+        J = torch.empty(n_obj, dtype=torch.float64, device="cuda")
+        ops.fit_objective(batch, act, J=J, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            ops.fit_objective(batch, act, J=J, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 3 / 1e3
+        out[f"objective_{act}"] = {"thetas": n_obj, "ms": round(t * 1e3, 3), "J_per_s": round(n_obj / t, 1)}
+    for act, obj in PAPER_THETA:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        best, _, _ = ops.fit_anneal(act, objective=obj, chains=chains, iters=iters, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        b = best.cpu().tolist()
+        Jp = float(gfit.objective(PAPER_THETA[(act, obj)], act, objective=obj)[0])
+        out[f"anneal_{act}_{obj}"] = {
+            "seconds": round(t, 3), "J_evals_per_s": round(chains * (iters + 1) / t, 1),
+            "J": b[-1], "J_paper": Jp, "J_over_paper": round(b[-1] / Jp, 6),
+            "a": [round(v, 6) for v in b[:2]], "c": [round(v, 6) for v in b[2:5]]}
+    if cpu:
+        from oracle import fit as ofit
+        n, t0 = 0, time.perf_counter()
+        rng = np.random.default_rng(1)
+        while time.perf_counter() - t0 < 3.0:
+            for act in ("gelu", "silu"):
+                ofit.objective(act, 2, np.array(PAPER_THETA[(act, "h")]) + 0.05 * rng.standard_normal(5))
+                n += 1
+        el = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(n / el, 2), "unit": "J evals/s", "cores": 1, "kind": "oracle",
+                               "sample": f"{n} objective evaluations (GELU and SiLU alternating, QUADPACK via "
+                                         f"scipy.integrate.quad) in {el:.1f} s"}
     return out
 
 
@@ -540,7 +604,9 @@ def main():
 
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
     block = block_section(cfg, R, dev) if rank == 0 else None
-    step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink)
+    step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink, peak)
+    fitter = fitter_section(stream, cpu=(world == 1 and not args.no_cpu_baseline)) if (
+        rank == 0 and not args.no_fitter) else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -567,6 +633,7 @@ def main():
             "reswiglu2": swiglu,
             "activation_bytes_saved_per_block": block,
             "stepact": step_k,
+            "fitter": fitter,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -67,7 +67,8 @@ typedef enum {
   LMBP_ERR_EPS = 4,
   LMBP_ERR_CUDA = 5,
   LMBP_ERR_KIND = 6,
-  LMBP_ERR_TABLE = 7
+  LMBP_ERR_TABLE = 7,
+  LMBP_ERR_ARG = 8
 } lmbp_status;
 
 typedef enum { LMBP_GELU = 0, LMBP_SILU = 1 } lmbp_act_kind;
@@ -202,6 +203,57 @@ LMBP_API int stepact_fwd(int act, int k, const double *thresholds, const void *x
                          int64_t rows, int64_t cols, int dtype, void *stream);
 LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint8_t *codes, void *dx,
                          int64_t rows, int64_t cols, int dtype, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Offline coefficient fitter: the step tables above are
+ * the minimisers of App. E's objective (Eq. 15, P:L1009-1065 GELU,
+ * P:L1086-1142 SiLU)
+ *     J(a, c) = int_A^B (h(x) - h~_{a,c}(x))^2 dx,
+ *     h~_{a,c}(x) = sum_{i<m} a_i ReLU(x - c_i) + (1 - sum a) ReLU(x - c_m)
+ * (Eq. 14, m = 2^k - 1 ReLUs), or of App. I's derivative
+ * objective (Eq. 17: h', h~' in place of h, h~), found by
+ * simulated annealing from many initialisations.
+ *
+ * theta: binary64 (a_1 .. a_{m-1}, c_1 .. c_m), P = 2m - 1 values; for k = 2
+ *   exactly the paper's five scalars (a1, a2, c1, c2, c3).
+ * act: LMBP_GELU / LMBP_SILU.  objective: LMBP_FIT_H (Eq. 15) or LMBP_FIT_DH
+ *   (Eq. 17).  k: 1..4.  eps: the tail tolerance that fixes [A, B]
+ *   (lmbp_fit_bounds; the paper uses 1e-8).
+ * Arithmetic: binary64 throughout; the integral is a composite 16-point
+ *   Gauss-Legendre rule on panels of length <= 2 between the sorted kinks.
+ * Errors: act / objective unknown -> LMBP_ERR_KIND; k outside 1..4 or
+ *   n < 0 -> LMBP_ERR_SHAPE; eps not in (0, 1) -> LMBP_ERR_EPS; NULL pointer
+ *   with work to do -> LMBP_ERR_NULLPTR; bad annealing schedule (chains < 1,
+ *   iters < 0, t0 / t1 / step0 / step1 not finite and > 0) -> LMBP_ERR_ARG;
+ *   launch failure -> LMBP_ERR_CUDA.  Deterministic for a given seed.
+ * ------------------------------------------------------------------------- */
+typedef enum { LMBP_FIT_H = 0, LMBP_FIT_DH = 1 } lmbp_fit_objective_kind;
+
+/* Host only: the truncated interval [A, B] of App. E for tail tolerance eps:
+ * GELU B = -A = sqrt(-2 ln eps); SiLU B = -A = -2 ln(eps / 2)
+ * (P:L1123).  A, B: HOST pointers. */
+LMBP_API int lmbp_fit_bounds(int act, double eps, double *A, double *B);
+
+/* J for n parameter vectors: theta DEVICE [n, P] row-major, J DEVICE [n].
+ * A J that is NaN (non-finite theta) is returned as +inf. */
+LMBP_API int lmbp_fit_objective(int act, int objective, int k, double eps, const double *theta, double *J,
+                                int64_t n, void *stream);
+
+/* Simulated annealing, one chain per GPU thread.  Chain i starts from init
+ * (DEVICE [P], shared by every chain; NULL = a random start per chain:
+ * weights around 1/m, thresholds uniform in [A/2, B/2]), then for `iters`
+ * steps perturbs one coordinate (cyclically) by a Gaussian of scale
+ * step(t) x (1 for weights, (B - A)/8 for thresholds) and accepts by the
+ * Metropolis rule at temperature T(t); T and step fall geometrically from
+ * (t0, step0) to (t1, step1).  Random numbers: a counter-based generator of
+ * (seed, chain, step), so results do not depend on the launch shape.
+ * Outputs (DEVICE, caller-owned): chain_theta [chains, P] and chain_J [chains]
+ * = each chain's best point, canonical (ReLUs sorted by threshold), and its
+ * J; best [P + 1] = the best chain's theta followed by its J (ties -> lowest
+ * chain index). */
+LMBP_API int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *init, int64_t chains,
+                             int64_t iters, uint64_t seed, double t0, double t1, double step0, double step1,
+                             double *chain_theta, double *chain_J, double *best, void *stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -12,6 +12,7 @@ import os
 from .build import LIB
 
 _p, _i64, _i32, _f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+_f64, _u64 = ctypes.c_double, ctypes.c_uint64
 
 # name -> (restype, argtypes); mirrors include/lmbp.h
 SIGNATURES = {
@@ -32,10 +33,15 @@ SIGNATURES = {
     "stepact_fwd": (_i32, [_i32, _i32, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "stepact_bwd": (_i32, [_i32, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "reswiglu2_bwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "lmbp_fit_bounds": (_i32, [_i32, _f64, _p, _p]),
+    "lmbp_fit_objective": (_i32, [_i32, _i32, _i32, _f64, _p, _p, _i64, _p]),
+    "lmbp_fit_anneal": (_i32, [_i32, _i32, _i32, _f64, _p, _i64, _i64, _u64, _f64, _f64, _f64, _f64, _p, _p, _p,
+                               _p]),
 }
 
 (LMBP_OK, LMBP_ERR_NULLPTR, LMBP_ERR_SHAPE, LMBP_ERR_DTYPE, LMBP_ERR_EPS, LMBP_ERR_CUDA, LMBP_ERR_KIND,
- LMBP_ERR_TABLE) = range(8)
+ LMBP_ERR_TABLE, LMBP_ERR_ARG) = range(9)
+LMBP_FIT_H, LMBP_FIT_DH = 0, 1
 LMBP_F32, LMBP_BF16, LMBP_F16 = 0, 1, 2
 LMBP_GELU, LMBP_SILU = 0, 1
 

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "liblmbp.so")
-SOURCES = ["abi.cu", "act.cu", "norm.cu", "swiglu.cu", "stepact.cu"]
+SOURCES = ["abi.cu", "act.cu", "norm.cu", "swiglu.cu", "stepact.cu", "fit.cu"]
 HEADERS = ["common.cuh", "constants.cuh", "kernels.h", "act_math.cuh", "ew_pipeline.cuh", os.path.join("..", "..", "include", "lmbp.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -136,6 +136,27 @@ static int stepact_bwd_entry(int k, const double *lvl, const void *dy, const uin
   return status_of(stepact_bwd(dtype, t, dy, codes, dx, rows * cols, static_cast<cudaStream_t>(stream)));
 }
 
+static bool fit_bounds(int act, double eps, double *A, double *B) {
+  if (!(eps > 0.0 && eps < 1.0)) return false;
+  const double b = act == kActGelu ? std::sqrt(-2.0 * std::log(eps)) : -2.0 * std::log(eps / 2.0);
+  *A = -b;
+  *B = b;
+  return true;
+}
+
+static int fit_spec(int act, int objective, int k, double eps, FitSpec *s) {
+  if (act != LMBP_GELU && act != LMBP_SILU) return LMBP_ERR_KIND;
+  if (objective != LMBP_FIT_H && objective != LMBP_FIT_DH) return LMBP_ERR_KIND;
+  if (k < 1 || k > 4) return LMBP_ERR_SHAPE;
+  if (!fit_bounds(act, eps, &s->A, &s->B)) return LMBP_ERR_EPS;
+  s->act = act == LMBP_GELU ? kActGelu : kActSilu;
+  s->obj = objective;
+  s->panel = 2.0;
+  return LMBP_OK;
+}
+
+static bool pos_finite(double v) { return std::isfinite(v) && v > 0.0; }
+
 }  // namespace lmbp
 
 extern "C" {
@@ -157,6 +178,7 @@ const char *lmbp_status_string(int status) {
     case LMBP_ERR_CUDA: return "LMBP_ERR_CUDA: kernel launch failed (cudaGetLastError)";
     case LMBP_ERR_KIND: return "LMBP_ERR_KIND: unknown activation kind";
     case LMBP_ERR_TABLE: return "LMBP_ERR_TABLE: k not in {1, 2, 4}, or thresholds not finite and strictly increasing, or levels not finite";
+    case LMBP_ERR_ARG: return "LMBP_ERR_ARG: invalid annealing schedule (chains < 1, iters < 0, or t0/t1/step0/step1 not finite and > 0)";
     default: return "LMBP: unknown status";
   }
 }
@@ -223,6 +245,38 @@ int stepact_fwd(int act, int k, const double *thresholds, const void *x, void *y
 int stepact_bwd(int k, const double *levels, const void *dy, const uint8_t *codes, void *dx, int64_t rows,
                 int64_t cols, int dtype, void *stream) {
   return lmbp::stepact_bwd_entry(k, levels, dy, codes, dx, rows, cols, dtype, stream);
+}
+
+int lmbp_fit_bounds(int act, double eps, double *A, double *B) {
+  if (act != LMBP_GELU && act != LMBP_SILU) return LMBP_ERR_KIND;
+  if (!A || !B) return LMBP_ERR_NULLPTR;
+  return lmbp::fit_bounds(act == LMBP_GELU ? lmbp::kActGelu : lmbp::kActSilu, eps, A, B) ? LMBP_OK : LMBP_ERR_EPS;
+}
+
+int lmbp_fit_objective(int act, int objective, int k, double eps, const double *theta, double *J, int64_t n,
+                       void *stream) {
+  lmbp::FitSpec s{};
+  int st = lmbp::fit_spec(act, objective, k, eps, &s);
+  if (st != LMBP_OK) return st;
+  if (n < 0) return LMBP_ERR_SHAPE;
+  if (n == 0) return LMBP_OK;
+  if (!theta || !J) return LMBP_ERR_NULLPTR;
+  return lmbp::status_of(lmbp::fit_objective(s, k, theta, J, n, static_cast<cudaStream_t>(stream)));
+}
+
+int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *init, int64_t chains, int64_t iters,
+                    uint64_t seed, double t0, double t1, double step0, double step1, double *chain_theta,
+                    double *chain_J, double *best, void *stream) {
+  lmbp::FitSpec s{};
+  int st = lmbp::fit_spec(act, objective, k, eps, &s);
+  if (st != LMBP_OK) return st;
+  if (chains < 1 || iters < 0 || !lmbp::pos_finite(t0) || !lmbp::pos_finite(t1) || !lmbp::pos_finite(step0) ||
+      !lmbp::pos_finite(step1))
+    return LMBP_ERR_ARG;
+  if (!chain_theta || !chain_J || !best) return LMBP_ERR_NULLPTR;
+  lmbp::AnnealCfg a{chains, iters, seed, t0, t1, step0, step1};
+  return lmbp::status_of(
+      lmbp::fit_anneal(s, k, a, init, chain_theta, chain_J, best, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

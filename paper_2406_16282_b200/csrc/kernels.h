@@ -29,4 +29,20 @@ cudaError_t swiglu_fwd(int dtype, const void *g, const void *u, void *h, void *a
 cudaError_t swiglu_bwd(int dtype, const void *dh, const void *u, const void *a, const uint8_t *codes, void *dg,
                        void *du, int64_t n, cudaStream_t s);
 
+// Coefficient fitter (fit.cu).
+struct FitSpec {
+  int act;       // kActGelu / kActSilu
+  int obj;       // 0: int (h - h~)^2 (Eq. 15), 1: int (h' - h~')^2 (Eq. 17)
+  double A, B;   // truncated interval (App. E tail bounds)
+  double panel;  // longest Gauss-Legendre panel
+};
+struct AnnealCfg {
+  int64_t chains, iters;
+  uint64_t seed;
+  double t0, t1, step0, step1;
+};
+cudaError_t fit_objective(const FitSpec &s, int k, const double *theta, double *J, int64_t n, cudaStream_t st);
+cudaError_t fit_anneal(const FitSpec &s, int k, const AnnealCfg &a, const double *init, double *chain_theta,
+                       double *chain_J, double *best, cudaStream_t st);
+
 }  // namespace lmbp

@@ -247,3 +247,59 @@ def stepact_bwd(dy, codes, k: int, levels, dx=None, stream=None):
     check("stepact_bwd", lib().stepact_bwd(int(k), ptr, dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols,
                                            _dtype(dy), _stream(stream)))
     return dx
+
+
+# ---------------------------------------------------------------------------
+# Offline coefficient fitter (lmbp.h lmbp_fit_*)
+# ---------------------------------------------------------------------------
+_ACT = {"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}
+_OBJ = {"h": _lib.LMBP_FIT_H, "dh": _lib.LMBP_FIT_DH}
+
+
+def fit_n_params(k: int) -> int:
+    """2 m - 1 parameters (m - 1 weights, m thresholds), m = 2^k - 1."""
+    return 2 * ((1 << int(k)) - 1) - 1
+
+
+def fit_bounds(act: str, eps: float = 1e-8):
+    """[A, B] of App. E for tail tolerance eps (host only)."""
+    import ctypes
+    A, B = ctypes.c_double(), ctypes.c_double()
+    check("lmbp_fit_bounds", lib().lmbp_fit_bounds(_ACT[act], float(eps), ctypes.byref(A), ctypes.byref(B)))
+    return A.value, B.value
+
+
+def fit_objective(theta, act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, J=None, stream=None):
+    """J(theta) for every row of a CUDA float64 tensor theta [n, P]."""
+    _need(theta, "theta")
+    P = fit_n_params(k)
+    if theta.dtype != torch.float64 or theta.dim() != 2 or theta.shape[1] != P:
+        raise ValueError(f"theta must be float64 [n, {P}]")
+    n = theta.shape[0]
+    J = torch.empty(n, dtype=torch.float64, device=theta.device) if J is None else _need(J, "J")
+    if J.dtype != torch.float64 or J.numel() != n:
+        raise ValueError("J must be float64 [n]")
+    check("lmbp_fit_objective", lib().lmbp_fit_objective(_ACT[act], _OBJ[objective], int(k), float(eps),
+                                                         theta.data_ptr(), J.data_ptr(), n, _stream(stream)))
+    return J
+
+
+def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, chains: int = 148 * 128,
+               iters: int = 3000, seed: int = 2406, t0: float = 1e-3, t1: float = 1e-12, step0: float = 0.3,
+               step1: float = 1e-6, init=None, device="cuda", stream=None):
+    """Simulated annealing on the GPU, one chain per thread.  Returns
+    (best [P + 1] = theta then J, chain_theta [chains, P], chain_J [chains]),
+    all CUDA float64 tensors."""
+    P = fit_n_params(k)
+    if init is not None:
+        _need(init, "init")
+        if init.dtype != torch.float64 or init.numel() != P:
+            raise ValueError(f"init must be float64 [{P}]")
+    chain_theta = torch.empty(chains, P, dtype=torch.float64, device=device)
+    chain_J = torch.empty(chains, dtype=torch.float64, device=device)
+    best = torch.empty(P + 1, dtype=torch.float64, device=device)
+    check("lmbp_fit_anneal", lib().lmbp_fit_anneal(
+        _ACT[act], _OBJ[objective], int(k), float(eps), None if init is None else init.data_ptr(), int(chains),
+        int(iters), int(seed) & (2 ** 64 - 1), float(t0), float(t1), float(step0), float(step1),
+        chain_theta.data_ptr(), chain_J.data_ptr(), best.data_ptr(), _stream(stream)))
+    return best, chain_theta, chain_J

@@ -59,7 +59,7 @@ def test_step_table_is_exact_rounding_of_paper_constants(kind):
 
 
 def test_status_strings():
-    for st in range(8):
+    for st in range(9):
         assert _lib.status_string(st).startswith("LMBP")
     assert "unknown" in _lib.status_string(99)
 
@@ -135,3 +135,38 @@ def test_product_package_does_not_import_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
                 assert not re.search(r"#\s*include\s*[<\"].*oracle", src), f
                 assert "liboracle" not in src, f
+
+
+def test_fit_bounds_and_validation_without_device_work():
+    """Coefficient fitter (NEXT #4): host-only bounds equal the paper's
+    formulas as the oracle implements them; validation precedes device work."""
+    from oracle import fit as ofit
+    L = _lib.lib()
+    S = _lib
+    for act in ("gelu", "silu"):
+        for eps in (1e-8, 1e-6, 0.5):
+            A, B = ops.fit_bounds(act, eps)
+            Ao, Bo = ofit.tail_bounds(act, eps)
+            assert A == pytest.approx(Ao, rel=1e-15) and B == pytest.approx(Bo, rel=1e-15)
+    fake = ctypes.c_void_p(0x1000)
+    assert L.lmbp_fit_bounds(7, 1e-8, fake, fake) == S.LMBP_ERR_KIND
+    assert L.lmbp_fit_bounds(0, 0.0, ctypes.byref(ctypes.c_double()), ctypes.byref(ctypes.c_double())) == S.LMBP_ERR_EPS
+    assert L.lmbp_fit_objective(5, 0, 2, 1e-8, fake, fake, 1, None) == S.LMBP_ERR_KIND
+    assert L.lmbp_fit_objective(0, 2, 2, 1e-8, fake, fake, 1, None) == S.LMBP_ERR_KIND
+    assert L.lmbp_fit_objective(0, 0, 0, 1e-8, fake, fake, 1, None) == S.LMBP_ERR_SHAPE
+    assert L.lmbp_fit_objective(0, 0, 5, 1e-8, fake, fake, 1, None) == S.LMBP_ERR_SHAPE
+    assert L.lmbp_fit_objective(0, 0, 2, float("nan"), fake, fake, 1, None) == S.LMBP_ERR_EPS
+    assert L.lmbp_fit_objective(0, 0, 2, 1.0, fake, fake, 1, None) == S.LMBP_ERR_EPS
+    assert L.lmbp_fit_objective(0, 0, 2, 1e-8, fake, fake, -1, None) == S.LMBP_ERR_SHAPE
+    assert L.lmbp_fit_objective(0, 0, 2, 1e-8, None, fake, 1, None) == S.LMBP_ERR_NULLPTR
+    assert L.lmbp_fit_objective(0, 0, 2, 1e-8, None, None, 0, None) == S.LMBP_OK
+    args = dict(t0=1e-3, t1=1e-9, s0=0.3, s1=1e-6)
+    def ann(chains=4, iters=10, t0=1e-3, t1=1e-9, s0=0.3, s1=1e-6, ptr=fake):
+        return L.lmbp_fit_anneal(0, 0, 2, 1e-8, None, chains, iters, 1, t0, t1, s0, s1, ptr, ptr, ptr, None)
+    assert ann(chains=0) == S.LMBP_ERR_ARG
+    assert ann(iters=-1) == S.LMBP_ERR_ARG
+    for bad in (0.0, -1.0, float("inf"), float("nan")):
+        for key in args:
+            kw = dict(args); kw[key] = bad
+            assert ann(**kw) == S.LMBP_ERR_ARG
+    assert ann(ptr=None) == S.LMBP_ERR_NULLPTR
