@@ -242,10 +242,13 @@ LMBP_API int lmbp_fit_objective(int act, int objective, int k, double eps, const
 /* Simulated annealing, one chain per GPU thread.  Chain i starts from init
  * (DEVICE [P], shared by every chain; NULL = a random start per chain:
  * weights around 1/m, thresholds uniform in [A/2, B/2]), then for `iters`
- * steps perturbs one coordinate (cyclically) by a Gaussian of scale
- * step(t) x (1 for weights, (B - A)/8 for thresholds) and accepts by the
- * Metropolis rule at temperature T(t); T and step fall geometrically from
- * (t0, step0) to (t1, step1).  Random numbers: a counter-based generator of
+ * steps perturbs one coordinate j (cyclically) by sigma_j N(0, 1) and
+ * accepts with probability min(1, exp(-(J' - J) / (T J))) (Metropolis at a
+ * temperature relative to the current J), T falling
+ * geometrically from t0 to t1.  sigma_j adapts per coordinate (x1.25 on
+ * accept, x0.92 on reject) within [step1, 4 step0] x (1 for weights,
+ * (B - A)/8 for thresholds), starting at step0 x that scale.
+ * Random numbers: a counter-based generator of
  * (seed, chain, step), so results do not depend on the launch shape.
  * Outputs (DEVICE, caller-owned): chain_theta [chains, P] and chain_J [chains]
  * = each chain's best point, canonical (ReLUs sorted by threshold), and its
@@ -254,6 +257,17 @@ LMBP_API int lmbp_fit_objective(int act, int objective, int k, double eps, const
 LMBP_API int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *init, int64_t chains,
                              int64_t iters, uint64_t seed, double t0, double t1, double step0, double step1,
                              double *chain_theta, double *chain_J, double *best, void *stream);
+
+/* Local refinement of n starting points (e.g. every annealing chain's best):
+ * Levenberg-Marquardt on J with a central-difference gradient and Hessian
+ * (steps 1e-4 x (1 for weights, (B - A)/8 for thresholds)), Cholesky solve
+ * of (H + lambda diag H) d = -g, at most `iters` accepted steps; a step is
+ * taken only if J decreases, so J_out <= J(theta) for every row.
+ * theta DEVICE [n, P] (may alias theta_out); theta_out DEVICE [n, P]
+ * (canonical form), J_out DEVICE [n]; best DEVICE [P + 1] or NULL (as in
+ * lmbp_fit_anneal).  iters < 0 -> LMBP_ERR_ARG; n < 0 -> LMBP_ERR_SHAPE. */
+LMBP_API int lmbp_fit_refine(int act, int objective, int k, double eps, const double *theta, int64_t n,
+                             int64_t iters, double *theta_out, double *J_out, double *best, void *stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

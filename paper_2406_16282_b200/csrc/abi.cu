@@ -279,4 +279,17 @@ int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *ini
       lmbp::fit_anneal(s, k, a, init, chain_theta, chain_J, best, static_cast<cudaStream_t>(stream)));
 }
 
+int lmbp_fit_refine(int act, int objective, int k, double eps, const double *theta, int64_t n, int64_t iters,
+                    double *theta_out, double *J_out, double *best, void *stream) {
+  lmbp::FitSpec s{};
+  int st = lmbp::fit_spec(act, objective, k, eps, &s);
+  if (st != LMBP_OK) return st;
+  if (n < 0) return LMBP_ERR_SHAPE;
+  if (iters < 0) return LMBP_ERR_ARG;
+  if (n == 0) return LMBP_OK;
+  if (!theta || !theta_out || !J_out) return LMBP_ERR_NULLPTR;
+  return lmbp::status_of(lmbp::fit_refine(s, k, theta, n, iters, theta_out, J_out, best,
+                                          static_cast<cudaStream_t>(stream)));
+}
+
 }  // extern "C"

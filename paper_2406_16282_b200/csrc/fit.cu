@@ -56,7 +56,7 @@ __device__ __forceinline__ double dh_fn(int act, double x) {
 }
 
 // int_l^r f(x) dx, f = (h - alpha x - beta)^2 (obj 0) or (h' - alpha)^2 (obj 1).
-__device__ double integrate_piece(const FitSpec &s, double l, double r, double alpha, double beta) {
+__device__ __noinline__ double integrate_piece(const FitSpec &s, double l, double r, double alpha, double beta) {
   if (!(r > l)) return 0.0;
   const int np = max(1, (int)ceil((r - l) / s.panel));
   const double half = 0.5 * (r - l) / np;
@@ -125,7 +125,7 @@ __device__ double objective_t(const FitSpec &s, const double *th) {
   unpack_theta<M>(th, w, c);
   sort_pairs<M>(w, c);
   double J = 0.0, alpha = 0.0, beta = 0.0;
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j <= M; ++j) {
     const double l = j == 0 ? s.A : fmin(fmax(c[j - 1], s.A), s.B);
     const double r = j == M ? s.B : fmin(fmax(c[j], s.A), s.B);
@@ -181,11 +181,15 @@ __device__ __forceinline__ double gauss(uint64_t seed, uint64_t chain, uint64_t 
   return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
-// One annealing chain per thread.  Proposal: one coordinate per step
-// (cyclic), Gaussian with scale step(t) * (1 for weights, (B - A)/8 for
-// thresholds); Metropolis acceptance at temperature T(t); T and step decay
-// geometrically from (t0, step0) to (t1, step1).  Writes the chain's best
-// point (canonical form) and its J.
+// One annealing chain per thread.  Proposal: one coordinate j per step
+// (cyclic), theta_j += sigma_j N(0, 1).  Acceptance: Metropolis at a
+// temperature relative to the current objective, P = exp(-(J' - J) / (T J)),
+// T falling geometrically from t0 to t1.  The objective's curvature differs
+// by ~1e5 between coordinates (an outer threshold barely moves J, a weight
+// does), so each coordinate keeps its own step: sigma_j grows by 1.25 on an
+// accepted move and shrinks by 0.92 on a rejected one (equilibrium acceptance
+// ~27 %), within [step1, 4 step0] x (1 for weights, (B - A)/8 for thresholds).
+// Writes the chain's best point (canonical form) and its J.
 template <int M>
 __global__ void __launch_bounds__(128) fit_anneal_k(FitSpec s, AnnealCfg a, const double *init, double *chain_theta,
                                                      double *chain_J) {
@@ -207,22 +211,32 @@ __global__ void __launch_bounds__(128) fit_anneal_k(FitSpec s, AnnealCfg a, cons
     best[i] = th[i];
   }
   ctr = 1ull << 40;  // proposals draw from a separate counter range
+  double sig[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) sig[i] = a.step0 * (i < M - 1 ? 1.0 : cscale);
   double J = objective_t<M>(s, th);
   double bestJ = J;
-  const double lt = log(a.t1 / a.t0), ls = log(a.step1 / a.step0);
+  const double lt = log(a.t1 / a.t0);
   for (int64_t it = 0; it < a.iters; ++it) {
     const double frac = a.iters > 1 ? (double)it / (double)(a.iters - 1) : 1.0;
     const double T = a.t0 * exp(lt * frac);
-    const double step = a.step0 * exp(ls * frac);
     const int j = (int)(it % P);
-    const double d = step * (j < M - 1 ? 1.0 : cscale) * gauss(a.seed, ch, ctr);
+    const double g = gauss(a.seed, ch, ctr);
     const double u = u01(a.seed, ch, (1ull << 62) + ctr);
     ctr += 1;
-    double prop[P];
+    double prop[P], sj = 0.0;
 #pragma unroll
-    for (int i = 0; i < P; ++i) prop[i] = th[i] + (i == j ? d : 0.0);
+    for (int i = 0; i < P; ++i) {
+      prop[i] = th[i] + (i == j ? sig[i] * g : 0.0);
+      sj = i == j ? sig[i] : sj;
+    }
     const double Jp = objective_t<M>(s, prop);
-    if (Jp <= J || u < exp((J - Jp) / T)) {
+    const bool acc = Jp <= J || u < exp((J - Jp) / (T * J));
+    const double sc = j < M - 1 ? 1.0 : cscale;
+    sj = fmin(fmax(sj * (acc ? 1.25 : 0.92), a.step1 * sc), 4.0 * a.step0 * sc);
+#pragma unroll
+    for (int i = 0; i < P; ++i) sig[i] = i == j ? sj : sig[i];
+    if (acc) {
 #pragma unroll
       for (int i = 0; i < P; ++i) th[i] = prop[i];
       J = Jp;
@@ -238,6 +252,109 @@ __global__ void __launch_bounds__(128) fit_anneal_k(FitSpec s, AnnealCfg a, cons
 #pragma unroll
   for (int i = 0; i < P; ++i) chain_theta[ch * P + i] = out[i];
   chain_J[ch] = bestJ;
+}
+
+// Local refinement (Levenberg-Marquardt on J): SA settles slowly into the
+// bottom of SiLU's long, curved valley (the objective's curvature spans ~1e5
+// across coordinates and its valley is diagonal in (a, c)), so every chain's
+// best point is finished by damped Newton steps.  Gradient and Hessian by
+// central differences (2 P^2 evaluations per step) with steps 1e-4 x (1 for
+// weights, (B - A)/8 for thresholds); solve (H + lambda diag H) d = -g by
+// Cholesky; accept if J falls (lambda / 10), else lambda x 10; stop after
+// `iters` steps or when 12 damping increases in a row find no decrease.
+// Out-of-line objective for the refinement kernel: it is called 2 P^2 times
+// per step, and inlining it into the Hessian loops made ptxas take hours.
+template <int M>
+__device__ __noinline__ double objective_call(const FitSpec &s, const double *th) {
+  return objective_t<M>(s, th);
+}
+
+template <int P>
+__device__ bool cholesky_solve(const double *H, const double *g, double lam, double *d) {
+  double L[P * P];
+  for (int i = 0; i < P; ++i) {
+    for (int j = 0; j <= i; ++j) {
+      double v = H[i * P + j] + (i == j ? lam * fabs(H[i * P + i]) + 1e-300 : 0.0);
+      for (int q = 0; q < j; ++q) v -= L[i * P + q] * L[j * P + q];
+      if (i == j) {
+        if (!(v > 0.0)) return false;
+        L[i * P + i] = sqrt(v);
+      } else {
+        L[i * P + j] = v / L[j * P + j];
+      }
+    }
+  }
+  double y[P];
+  for (int i = 0; i < P; ++i) {
+    double v = -g[i];
+    for (int q = 0; q < i; ++q) v -= L[i * P + q] * y[q];
+    y[i] = v / L[i * P + i];
+  }
+  for (int i = P - 1; i >= 0; --i) {
+    double v = y[i];
+    for (int q = i + 1; q < P; ++q) v -= L[q * P + i] * d[q];
+    d[i] = v / L[i * P + i];
+  }
+  return true;
+}
+
+template <int M>
+__global__ void __launch_bounds__(128) fit_refine_k(FitSpec s, const double *in, int64_t n, int64_t iters,
+                                                     double *out, double *Jout) {
+  constexpr int P = 2 * M - 1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double cscale = (s.B - s.A) * 0.125;
+  double th[P], h[P], g[P], H[P * P], tp[P], d[P];
+  for (int i = 0; i < P; ++i) {
+    th[i] = in[t * P + i];
+    h[i] = 1e-4 * (i < M - 1 ? 1.0 : cscale);
+  }
+  double J = objective_call<M>(s, th);
+  double lam = 1e-3;
+  for (int64_t it = 0; it < iters && isfinite(J); ++it) {
+    for (int i = 0; i < P; ++i) tp[i] = th[i];
+    for (int i = 0; i < P; ++i) {
+      tp[i] = th[i] + h[i];
+      const double jp = objective_call<M>(s, tp);
+      tp[i] = th[i] - h[i];
+      const double jm = objective_call<M>(s, tp);
+      tp[i] = th[i];
+      g[i] = (jp - jm) / (2.0 * h[i]);
+      H[i * P + i] = (jp - 2.0 * J + jm) / (h[i] * h[i]);
+    }
+    for (int i = 0; i < P; ++i) {
+      for (int j = 0; j < i; ++j) {
+        double acc = 0.0;
+        for (int q = 0; q < 4; ++q) {
+          const double si = (q & 1) ? -1.0 : 1.0, sj = (q & 2) ? -1.0 : 1.0;
+          tp[i] = th[i] + si * h[i];
+          tp[j] = th[j] + sj * h[j];
+          acc += si * sj * objective_call<M>(s, tp);
+        }
+        tp[i] = th[i];
+        tp[j] = th[j];
+        H[i * P + j] = H[j * P + i] = acc / (4.0 * h[i] * h[j]);
+      }
+    }
+    bool moved = false;
+    for (int tries = 0; tries < 12 && !moved; ++tries, lam *= 10.0) {
+      if (!cholesky_solve<P>(H, g, lam, d)) continue;
+      for (int i = 0; i < P; ++i) tp[i] = th[i] + d[i];
+      const double Jn = objective_call<M>(s, tp);
+      if (Jn < J) {
+        for (int i = 0; i < P; ++i) th[i] = tp[i];
+        J = Jn;
+        moved = true;
+        lam = fmax(lam * 0.01, 1e-12);  // / 10 after the loop's x 10
+      }
+    }
+    if (!moved) break;
+  }
+  double o[P];
+  canonical<M>(th, o);
+  for (int i = 0; i < P; ++i) out[t * P + i] = o[i];
+  Jout[t] = J;
 }
 
 // best = (theta of the chain with the smallest J, J); ties -> lowest chain
@@ -296,7 +413,29 @@ cudaError_t anneal_m(const FitSpec &s, const AnnealCfg &a, const double *init, d
   return cudaGetLastError();
 }
 
+template <int M>
+cudaError_t refine_m(const FitSpec &s, const double *in, int64_t n, int64_t iters, double *out, double *Jout,
+                     double *best, cudaStream_t st) {
+  const int64_t blocks = (n + 127) / 128;
+  if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+  fit_refine_k<M><<<(int)blocks, 128, 0, st>>>(s, in, n, iters, out, Jout);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !best) return e;
+  fit_best_k<<<1, 1024, 0, st>>>(out, Jout, n, 2 * M - 1, best);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t fit_refine(const FitSpec &s, int k, const double *in, int64_t n, int64_t iters, double *out,
+                       double *Jout, double *best, cudaStream_t st) {
+  switch (k) {
+    case 1: return refine_m<1>(s, in, n, iters, out, Jout, best, st);
+    case 2: return refine_m<3>(s, in, n, iters, out, Jout, best, st);
+    case 3: return refine_m<7>(s, in, n, iters, out, Jout, best, st);
+    default: return refine_m<15>(s, in, n, iters, out, Jout, best, st);
+  }
+}
 
 cudaError_t fit_objective(const FitSpec &s, int k, const double *theta, double *J, int64_t n, cudaStream_t st) {
   switch (k) {

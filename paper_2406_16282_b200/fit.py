@@ -39,8 +39,16 @@ class Fit:
         return list(self.c), lv
 
 
-def fit(act: str, k: int = 2, objective: str = "h", **anneal_kw) -> Fit:
-    best, _, _ = ops.fit_anneal(act, k=k, objective=objective, **anneal_kw)
+def fit(act: str, k: int = 2, objective: str = "h", refine_iters: int = 40, **anneal_kw) -> Fit:
+    """Global search, then local refinement, both in GPU kernels with no host
+    round trip: simulated annealing from many random starts (P:L1050-1053,
+    "searching multiple times with different initialization"), then every
+    chain's best point finished by Levenberg-Marquardt (lmbp_fit_refine) and
+    the best refined point taken."""
+    best, chain_theta, chain_J = ops.fit_anneal(act, k=k, objective=objective, **anneal_kw)
+    if refine_iters > 0:
+        best, _, _ = ops.fit_refine(chain_theta, act, k=k, objective=objective,
+                                    eps=anneal_kw.get("eps", 1e-8), iters=refine_iters)
     b = best.double().cpu().tolist()
     m = (1 << k) - 1
     return Fit(act=act, k=k, objective=objective, a=b[:m - 1], c=b[m - 1:2 * m - 1], J=b[-1])

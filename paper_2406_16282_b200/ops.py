@@ -285,8 +285,8 @@ def fit_objective(theta, act: str, k: int = 2, objective: str = "h", eps: float 
 
 
 def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, chains: int = 148 * 128,
-               iters: int = 3000, seed: int = 2406, t0: float = 1e-3, t1: float = 1e-12, step0: float = 0.3,
-               step1: float = 1e-6, init=None, device="cuda", stream=None):
+               iters: int = 3000, seed: int = 2406, t0: float = 0.1, t1: float = 1e-9, step0: float = 0.3,
+               step1: float = 1e-9, init=None, device="cuda", stream=None):
     """Simulated annealing on the GPU, one chain per thread.  Returns
     (best [P + 1] = theta then J, chain_theta [chains, P], chain_J [chains]),
     all CUDA float64 tensors."""
@@ -303,3 +303,20 @@ def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, ch
         int(iters), int(seed) & (2 ** 64 - 1), float(t0), float(t1), float(step0), float(step1),
         chain_theta.data_ptr(), chain_J.data_ptr(), best.data_ptr(), _stream(stream)))
     return best, chain_theta, chain_J
+
+
+def fit_refine(theta, act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, iters: int = 40, stream=None):
+    """Levenberg-Marquardt refinement of every row of theta [n, P] (CUDA
+    float64).  Returns (best [P + 1], theta_out [n, P], J_out [n])."""
+    _need(theta, "theta")
+    P = fit_n_params(k)
+    if theta.dtype != torch.float64 or theta.dim() != 2 or theta.shape[1] != P:
+        raise ValueError(f"theta must be float64 [n, {P}]")
+    n = theta.shape[0]
+    out = torch.empty_like(theta)
+    J = torch.empty(n, dtype=torch.float64, device=theta.device)
+    best = torch.empty(P + 1, dtype=torch.float64, device=theta.device)
+    check("lmbp_fit_refine", lib().lmbp_fit_refine(_ACT[act], _OBJ[objective], int(k), float(eps), theta.data_ptr(),
+                                                   n, int(iters), out.data_ptr(), J.data_ptr(), best.data_ptr(),
+                                                   _stream(stream)))
+    return best, out, J
