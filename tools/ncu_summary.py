@@ -23,6 +23,11 @@ KEYS = {
     "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "lsu_pipe_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "fp64_inst_pct": "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "dfma_thread_inst": "sm__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "dadd_thread_inst": "sm__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "dmul_thread_inst": "sm__sass_thread_inst_executed_op_dmul_pred_on.sum",
     "registers": "launch__registers_per_thread",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
