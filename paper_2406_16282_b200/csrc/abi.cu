@@ -112,6 +112,11 @@ static int stepact_fwd_entry(int act, int k, const double *thr, const void *x, v
   for (int i = 0; i < (1 << k) - 1; ++i) {
     if (!std::isfinite(thr[i]) || (i > 0 && !(thr[i] > thr[i - 1]))) return LMBP_ERR_TABLE;
     t.thr[i] = rd32(thr[i]);
+    // RD_T(RD32(c)) == RD_T(c): every value of T is a binary32 value.
+    uint16_t h = 0;
+    if (dtype == LMBP_BF16) h = __bfloat16_as_ushort(__float2bfloat16_rd(t.thr[i]));
+    else if (dtype == LMBP_F16) h = __half_as_ushort(__float2half_rd(t.thr[i]));
+    t.thr2[i] = (uint32_t)h | ((uint32_t)h << 16);
   }
   if (rows == 0) return LMBP_OK;
   if (!x || !y || !codes) return LMBP_ERR_NULLPTR;

@@ -169,6 +169,7 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
 struct StepTable {
   float thr[15];
   float lvl[16];
+  uint32_t thr2[15];  // bf16 / fp16 launches: RD_T(thr) duplicated into both halves (packed compares)
   int k;
 };
 

@@ -41,6 +41,13 @@ struct EwParams {
 template <class Op, class = void> struct ParamsOf { using type = EwParams; };
 template <class Op> struct ParamsOf<Op, std::void_t<typename Op::Params>> { using type = typename Op::Params; };
 
+// Optional `static constexpr int kMinBlocks` (CTAs that must fit per SM;
+// default: no register cap beyond the CTA size).
+template <class Op, class = void> struct MinBlocksOf { static constexpr int value = 0; };
+template <class Op> struct MinBlocksOf<Op, std::void_t<decltype(Op::kMinBlocks)>> {
+  static constexpr int value = Op::kMinBlocks;
+};
+
 template <class Op> struct EwShape {
   static constexpr int kTile = Op::W * 32 * Op::U;  // vectors per tile
   static constexpr int kThreads = (Op::W + 1) * 32;
@@ -84,8 +91,21 @@ __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
 #define LMBP_EW_UNIT 1
 #endif
 
+// Optional per-CTA lookup table in shared memory: an Op with
+// `static constexpr int kLut` and `static float lut_entry(const Params &, int)`
+// gets the filled table as a trailing `const float *` argument of apply().
+template <class Op, class = void> struct LutOf { static constexpr int value = 0; };
+template <class Op> struct LutOf<Op, std::void_t<decltype(Op::kLut)>> { static constexpr int value = Op::kLut; };
+
+template <class Op, class P, int NIN>
+__device__ __forceinline__ uint32_t apply_op(const uint4 (&v)[NIN], uint32_t c, int64_t i, const P &p,
+                                             const float *lut) {
+  if constexpr (LutOf<Op>::value > 0) return Op::apply(v, c, i, p, lut);
+  else return Op::apply(v, c, i, p);
+}
+
 template <class Op>
-__global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const typename ParamsOf<Op>::type p) {
+__global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value) ew_tma(const typename ParamsOf<Op>::type p) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Sh = EwShape<Op>;
   constexpr int W = Op::W, U = Op::U, S = Op::S, NIN = Op::kIn, TILE = Sh::kTile;
@@ -99,6 +119,13 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const typename P
   const int64_t ntiles = p.nvec / TILE;
   const int64_t nitems = ntiles + 1;                           // + the leftover pseudo-tile
 
+  constexpr int kLut = LutOf<Op>::value;
+  const float *lut = nullptr;
+  if constexpr (kLut > 0) {
+    __shared__ float lut_s[kLut];
+    if (threadIdx.x < kLut) lut_s[threadIdx.x] = Op::lut_entry(p, threadIdx.x);
+    lut = lut_s;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -163,7 +190,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const typename P
         uint4 v[NIN];
 #pragma unroll
         for (int m = 0; m < NIN; ++m) v[m] = ld_stream(p.in[m] + i);
-        const uint32_t co = Op::apply(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p);
+        const uint32_t co = apply_op<Op>(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p, lut);
         put_code<Op::kCodeOut>(p.codes_out, i, co);
       }
       if (threadIdx.x == 0) Op::tail(p);
@@ -186,7 +213,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads) ew_tma(const typename P
     const int64_t wbase = t * TILE + warp * (32 * U);
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const uint32_t co = Op::apply(v[j], c[j], wbase + j * 32 + lane, p);
+      const uint32_t co = apply_op<Op>(v[j], c[j], wbase + j * 32 + lane, p, lut);
       if constexpr (Op::kCodeOut > 0) put_code<Op::kCodeOut>(cstage + warp * Sh::kWarpCodeBytes, j * 32 + lane, co);
     }
     if constexpr (Op::kCodeOut > 0) {

@@ -17,6 +17,10 @@
 #include "ew_pipeline.cuh"
 #include "kernels.h"
 
+#ifndef LMBP_STEP_MINB4
+#define LMBP_STEP_MINB4 2
+#endif
+
 namespace lmbp {
 
 template <int K>
@@ -119,41 +123,99 @@ __global__ void __launch_bounds__(256) stepact_bwd_k(const T *dy, const uint8_t 
 // kVec k >= 8: every case except fp32 with k = 1, which keeps the simple
 // kernel).  Same per-element arithmetic as the simple kernel -> bitwise equal.
 // ---------------------------------------------------------------------------
-template <int K>
-__device__ __forceinline__ float level_sel(const float *L, uint32_t c) {
-  if constexpr (K == 1) {
-    return c ? L[1] : L[0];
-  } else if constexpr (K == 2) {
-    const float lo = (c & 1u) ? L[1] : L[0];
-    const float hi = (c & 1u) ? L[3] : L[2];
-    return (c & 2u) ? hi : lo;
-  } else {
-    float a[8], b[4], d[2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = (c & 1u) ? L[2 * i + 1] : L[2 * i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] = (c & 2u) ? a[2 * i + 1] : a[2 * i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) d[i] = (c & 4u) ? b[2 * i + 1] : b[2 * i];
-    return (c & 8u) ? d[1] : d[0];
-  }
-}
-
 struct StepEwParams : EwParams {
   StepTable tab;  // runtime step table
 };
 
+// Codes of one 16-byte vector by a branch-free binary search over the sorted
+// thresholds, bit by bit from the top: bit b of code = #{i : x > c_i} is
+// [x > c_(j 2^b + 2^b)] (1-based) where j holds the bits above b already
+// found (thresholds increasing, so the count is the position of x among them).
+// The candidate threshold for bit b is picked from 2^(K-1-b) candidates by a
+// mux tree on the higher bits' masks.  k compares per element instead of
+// 2^k - 1; for 16-bit types the compares are packed (HSET2: two elements per
+// instruction, masks 0xffff per half) and the mux is one LOP3 per node on
+// both halves at once.
+template <int K>
+__device__ __forceinline__ uint32_t bsearch_masks_16(uint32_t v, const uint32_t (&t)[15], bool bf16,
+                                                     uint32_t (&M)[K]) {
+#pragma unroll
+  for (int b = K - 1; b >= 0; --b) {
+    uint32_t cand[1 << (K - 1)];
+#pragma unroll
+    for (int j = 0; j < (1 << (K - 1 - b)); ++j) cand[j] = t[(2 * j + 1) * (1 << b) - 1];
+#pragma unroll
+    for (int q = b + 1, w = 1 << (K - 1 - b); q < K; ++q, w >>= 1) {
+#pragma unroll
+      for (int j = 0; j < w / 2; ++j) cand[j] = (M[q] & cand[2 * j + 1]) | (~M[q] & cand[2 * j]);
+    }
+    if (bf16)
+      M[b] = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162 *>(&v), *reinterpret_cast<const __nv_bfloat162 *>(&cand[0]));
+    else
+      M[b] = __hgt2_mask(*reinterpret_cast<const __half2 *>(&v), *reinterpret_cast<const __half2 *>(&cand[0]));
+  }
+  uint32_t z = 0;
+#pragma unroll
+  for (int b = 0; b < K; ++b) z |= M[b] & (0x10001u << b);
+  return z;  // element 2j's code at bits 0..K-1, element 2j+1's at 16..16+K-1
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t bsearch_code_f32(float x, const float (&t)[15]) {
+  bool M[K];
+  uint32_t code = 0;
+#pragma unroll
+  for (int b = K - 1; b >= 0; --b) {
+    float cand[1 << (K - 1)];
+#pragma unroll
+    for (int j = 0; j < (1 << (K - 1 - b)); ++j) cand[j] = t[(2 * j + 1) * (1 << b) - 1];
+#pragma unroll
+    for (int q = b + 1, w = 1 << (K - 1 - b); q < K; ++q, w >>= 1) {
+#pragma unroll
+      for (int j = 0; j < w / 2; ++j) cand[j] = M[q] ? cand[2 * j + 1] : cand[2 * j];
+    }
+    M[b] = x > cand[0];
+    code |= (uint32_t)M[b] << b;
+  }
+  return code;
+}
+
+template <typename T, int K>
+__device__ __forceinline__ uint32_t step_codes_vec(const uint4 &r, const float *f, const StepTable &tab) {
+  uint32_t W = 0;
+  if constexpr (Traits<T>::kVec == 4) {
+    float t[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) t[i] = i < (1 << K) - 1 ? tab.thr[i] : 0.0f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) W |= bsearch_code_f32<K>(f[e], t) << (K * e);
+  } else {
+    uint32_t t[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) t[i] = i < (1 << K) - 1 ? tab.thr2[i] : 0u;
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t M[K];
+      const uint32_t z = bsearch_masks_16<K>(w[j], t, std::is_same<T, __nv_bfloat16>::value, M);
+      W |= ((z & ((1u << K) - 1)) | ((z >> 16) << K)) << (2 * K * j);
+    }
+  }
+  return W;
+}
+
 template <typename T, int A, bool kPrecise, int K>
 struct StepFwdOp {
   using Params = StepEwParams;
+  // 2 CTAs / SM (<= 60 registers): at k = 4 the 15 hoisted packed thresholds
+  // would otherwise take the kernel to 72 registers and 1 CTA / SM.
+  static constexpr int kMinBlocks = K == 4 ? LMBP_STEP_MINB4 : 0;
   static constexpr int kVecT = Traits<T>::kVec;
   static constexpr int W = 16, U = 2, S = 4, kIn = 1, kCodeIn = 0, kCodeOut = kVecT * K / 8;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p) {
     float f[kVecT];
     Vec<T>::unpack(v[0], f);
-    uint32_t w = 0;
-#pragma unroll
-    for (int e = 0; e < kVecT; ++e) w |= step_code<K>(f[e], p.tab.thr) << (K * e);
+    const uint32_t w = step_codes_vec<T, K>(v[0], f, p.tab);
 #pragma unroll
     for (int e = 0; e < kVecT; e += 2) {
       const float2 r = act2_f<A, kPrecise>(make_float2(f[e], f[e + 1]));
@@ -184,15 +246,17 @@ struct StepBwdOp {
   using Params = StepEwParams;
   static constexpr int kVecT = Traits<T>::kVec;
   static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = kVecT * K / 8, kCodeOut = 0;
-  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const StepEwParams &p) {
+  // Levels in a shared-memory table: one conflict-free LDS per element (16
+  // words in 16 banks; equal codes broadcast) instead of a 2^k - 1 select tree.
+  static constexpr int kLut = 1 << K;
+  __device__ static float lut_entry(const StepEwParams &p, int i) { return p.tab.lvl[i]; }
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const StepEwParams &p,
+                                   const float *lut) {
     constexpr uint32_t kMask = (1u << K) - 1u;
-    float L[1 << K];
-#pragma unroll
-    for (int q = 0; q < (1 << K); ++q) L[q] = p.tab.lvl[q];
     float f[kVecT];
     Vec<T>::unpack(v[0], f);
 #pragma unroll
-    for (int e = 0; e < kVecT; ++e) f[e] = __fmul_rn(f[e], level_sel<K>(L, (c >> (K * e)) & kMask));
+    for (int e = 0; e < kVecT; ++e) f[e] = __fmul_rn(f[e], lut[(c >> (K * e)) & kMask]);
     st_stream(p.out[0] + i, Vec<T>::pack(f));
     return 0u;
   }

@@ -58,6 +58,11 @@ def main():
     y = ybuf[a.yoff:].view(x.dtype).view(x.shape)
     dx = torch.empty_like(dy)
     codes = torch.empty((R * F + 3) // 4, dtype=torch.uint8, device=dev)
+    codes4 = torch.empty((R * F + 1) // 2, dtype=torch.uint8, device=dev)
+    thr2 = (ctypes.c_double * 3)(-3.1858810036855245, -0.001178821281161997, 3.190832613414926)
+    lv2 = (ctypes.c_double * 4)(0.0, -0.04922261145617846, 1.0487405950855513, 1.0)
+    thr4 = (ctypes.c_double * 15)(*[-3.0 + 0.4 * i for i in range(15)])
+    lv4 = (ctypes.c_double * 16)(*[i / 15 for i in range(16)])
     xn = synth.norm_input(R, H, dt, device=dev)
     gn = synth.grad_input(R, H, dt, device=dev)
     yn, dxn = torch.empty_like(xn), torch.empty_like(gn)
@@ -69,7 +74,9 @@ def main():
     b = synth.ELEM_BYTES[dt]
     n = R * F
     nbytes = {"ncopy": 2 * b * R * H, "copy": 2 * b * n, "act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
-              "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R}
+              "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R,
+              "step2_fwd": 2 * b * n + (n + 3) // 4, "step4_fwd": 2 * b * n + (n + 1) // 2,
+              "step4_bwd": 2 * b * n + (n + 1) // 2}
     act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
     nrm = "msln" if cfg["norm"] == "ln" else "msrms"
     for name, path in libs.items():
@@ -84,8 +91,16 @@ def main():
             "norm_bwd": lambda: getattr(L, nrm + "_bwd")(gn.data_ptr(), yn.data_ptr(), rstd.data_ptr(), dxn.data_ptr(),
                                                          R, H, DT[dt], sp),
         }
+        ak = 0 if cfg["act"] == "gelu" else 1
+        calls["step2_fwd"] = lambda: L.stepact_fwd(ak, 2, ctypes.addressof(thr2), x.data_ptr(), y.data_ptr(),
+                                                   codes.data_ptr(), R, F, DT[dt], sp)
+        calls["step4_fwd"] = lambda: L.stepact_fwd(ak, 4, ctypes.addressof(thr4), x.data_ptr(), y.data_ptr(),
+                                                   codes4.data_ptr(), R, F, DT[dt], sp)
+        calls["step4_bwd"] = lambda: L.stepact_bwd(4, ctypes.addressof(lv4), dy.data_ptr(), codes4.data_ptr(),
+                                                   dx.data_ptr(), R, F, DT[dt], sp)
         calls["act_fwd"]()
         calls["norm_fwd"]()
+        calls["step4_fwd"]()
         for k in a.kernels.split(","):
             for _ in range(3):
                 calls[k]()
