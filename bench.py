@@ -206,13 +206,24 @@ def calibrate_rows(cfg, eps, target_s):
     return max(8, min(cfg["R"], int(rows * target_s / max(sec, 1e-4))))
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(cfg, eps, target_s):
     rows = calibrate_rows(cfg, eps, target_s)
     sec, nbytes, threads = oracle_step_sample(cfg, rows, eps)
     return {"value": round(nbytes / sec / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{rows} of {cfg['R']} rows of {cfg['desc']}: norm fwd+bwd and act fwd+bwd, float64 "
                       f"oracle incl. storage decode/encode, {sec:.2f} s",
-            "seconds": round(sec, 3), "rows": rows}
+            "seconds": round(sec, 3), "rows": rows, "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
 
 
 def run_reference(args):

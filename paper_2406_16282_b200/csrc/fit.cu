@@ -39,26 +39,36 @@ __device__ __forceinline__ double gl_x(int i) { return __longlong_as_double((lon
 __device__ __forceinline__ double gl_w(int i) { return __longlong_as_double((long long)cGLW[i]); }
 
 // h and h' in binary64.
-__device__ __forceinline__ double h_fn(int act, double x) {
-  if (act == kActGelu) return 0.5 * x * erfc(-x * 0.70710678118654752440);
-  const double e = exp(-fabs(x));            // SiLU, stable in both tails
-  return x >= 0.0 ? x / (1.0 + e) : x * e / (1.0 + e);
+template <int ACT>
+__device__ __forceinline__ double h_fn(double x) {
+  if constexpr (ACT == kActGelu) {
+    return 0.5 * x * erfc(-x * 0.70710678118654752440);
+  } else {
+    const double e = exp(-fabs(x));            // SiLU, stable in both tails
+    return x >= 0.0 ? x / (1.0 + e) : x * e / (1.0 + e);
+  }
 }
 
-__device__ __forceinline__ double dh_fn(int act, double x) {
-  if (act == kActGelu)
+template <int ACT>
+__device__ __forceinline__ double dh_fn(double x) {
+  if constexpr (ACT == kActGelu) {
     return 0.5 * erfc(-x * 0.70710678118654752440) + x * exp(-0.5 * x * x) * 0.39894228040143267794;
-  const double e = exp(-fabs(x));
-  const double r = 1.0 / (1.0 + e);
-  const double s = x >= 0.0 ? r : e * r;     // sigma(x)
-  const double sc = x >= 0.0 ? e * r : r;    // 1 - sigma(x), no cancellation
-  return s + x * s * sc;
+  } else {
+    const double e = exp(-fabs(x));
+    const double r = 1.0 / (1.0 + e);
+    const double s = x >= 0.0 ? r : e * r;     // sigma(x)
+    const double sc = x >= 0.0 ? e * r : r;    // 1 - sigma(x), no cancellation
+    return s + x * s * sc;
+  }
 }
 
-// int_l^r f(x) dx, f = (h - alpha x - beta)^2 (obj 0) or (h' - alpha)^2 (obj 1).
-__device__ __noinline__ double integrate_piece(const FitSpec &s, double l, double r, double alpha, double beta) {
+// int_l^r f(x) dx, f = (h - alpha x - beta)^2 (OBJ 0) or (h' - alpha)^2 (OBJ 1).
+// One out-of-line specialisation per (activation, objective): a launch only
+// ever runs one of them, so the instruction cache holds one small body.
+template <int ACT, int OBJ>
+__device__ __noinline__ double integrate_piece_t(double l, double r, double alpha, double beta, double panel) {
   if (!(r > l)) return 0.0;
-  const int np = max(1, (int)ceil((r - l) / s.panel));
+  const int np = max(1, (int)ceil((r - l) / panel));
   const double half = 0.5 * (r - l) / np;
   double acc = 0.0;
   for (int p = 0; p < np; ++p) {
@@ -69,18 +79,26 @@ __device__ __noinline__ double integrate_piece(const FitSpec &s, double l, doubl
       const double dx = half * gl_x(i);
       const double x0 = mid - dx, x1 = mid + dx;
       double f0, f1;
-      if (s.obj == 0) {
-        f0 = h_fn(s.act, x0) - fma(alpha, x0, beta);
-        f1 = h_fn(s.act, x1) - fma(alpha, x1, beta);
+      if constexpr (OBJ == 0) {
+        f0 = h_fn<ACT>(x0) - fma(alpha, x0, beta);
+        f1 = h_fn<ACT>(x1) - fma(alpha, x1, beta);
       } else {
-        f0 = dh_fn(s.act, x0) - alpha;
-        f1 = dh_fn(s.act, x1) - alpha;
+        f0 = dh_fn<ACT>(x0) - alpha;
+        f1 = dh_fn<ACT>(x1) - alpha;
       }
       pa = fma(gl_w(i), fma(f0, f0, f1 * f1), pa);
     }
     acc += pa;
   }
   return acc * half;
+}
+
+__device__ __forceinline__ double integrate_piece(const FitSpec &s, double l, double r, double alpha, double beta) {
+  if (s.act == kActGelu)
+    return s.obj == 0 ? integrate_piece_t<kActGelu, 0>(l, r, alpha, beta, s.panel)
+                      : integrate_piece_t<kActGelu, 1>(l, r, alpha, beta, s.panel);
+  return s.obj == 0 ? integrate_piece_t<kActSilu, 0>(l, r, alpha, beta, s.panel)
+                    : integrate_piece_t<kActSilu, 1>(l, r, alpha, beta, s.panel);
 }
 
 // Sort the ReLUs by threshold (weights travel with them); fully unrolled so

@@ -20,7 +20,8 @@ for dt in ("f32", "bf16", "f16"):
             bwd(dy, c)
         h, a, c = P.reswiglu2_fwd(x, dy)
         P.reswiglu2_bwd(dy, dy, a, c)
-        for k, thr, lv in ((1, [0.0], [0.0, 1.0]), (2, tables.REGELU2["c"], tables.levels(tables.REGELU2))):
+        for k, thr, lv in ((1, [0.0], [0.0, 1.0]), (2, tables.REGELU2["c"], tables.levels(tables.REGELU2)),
+                           (4, [-3.0 + 0.4 * i for i in range(15)], [i / 15 for i in range(16)])):
             y, c = P.stepact_fwd(x, "gelu", k, thr)
             P.stepact_bwd(dy, c, k, lv)
     for (R, H) in ((3, 7), (33, 768), (9, 4096), (5, 5120), (2, 40000)):
@@ -29,5 +30,14 @@ for dt in ("f32", "bf16", "f16"):
         for fwd, bwd in ((P.msln_fwd, P.msln_bwd), (P.msrms_fwd, P.msrms_bwd)):
             yn, r = fwd(xn, 1e-6)
             bwd(gn, yn, r)
+# coefficient fitter (fp64): objective for k = 1..3, a short anneal + refine
+for act in ("gelu", "silu"):
+    for k in (1, 2, 3):
+        P_ = P.ops.fit_n_params(k)
+        th = torch.randn(67, P_, dtype=torch.float64, device=dev)
+        P.ops.fit_objective(th, act, k=k)
+        P.ops.fit_objective(th, act, k=k, objective="dh")
+    best, cth, cj = P.ops.fit_anneal(act, chains=150, iters=20)
+    P.ops.fit_refine(cth, act, iters=2)
 torch.cuda.synchronize()
 print("sanitize driver ok")
