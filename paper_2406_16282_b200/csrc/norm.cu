@@ -378,13 +378,14 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t row_bytes = (size_t)nvec * 16;
   const size_t stage_bytes = row_bytes * NIN;
-  // layout: stages | clc response (16 B) | full[S] empty[S] clc_bar | slot[S] | red
+  // layout: stages | clc response (16 B) | full[S] empty[S] clc_bar | slot[S] | red | rslot[S]
   uint4 *clc_resp = reinterpret_cast<uint4 *>(smem + (size_t)stages * stage_bytes);  // 16-byte aligned
   uint64_t *full = reinterpret_cast<uint64_t *>(clc_resp + 1);
   uint64_t *empty = full + stages;
   uint64_t *clc_bar = empty + stages;
   int64_t *slot = reinterpret_cast<int64_t *>(clc_bar + 1);
   float2 *red = reinterpret_cast<float2 *>(slot + stages);     // [2 parities][2 reductions][16 warps]
+  float *rslot = reinterpret_cast<float *>(red + 64);          // backward: the stage row's rstd
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -398,6 +399,11 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
   if (warp == W) {  // producer
     if (lane == 0) {
       int64_t row = blockIdx.x;
+      // backward: the producer loads the row's rstd (issued a row ahead, so
+      // the load's latency hides behind the stage wait) and hands it over in
+      // the stage's slot; the consumers never wait on global memory.
+      float rnext = 0.0f;
+      if constexpr (!kFwd) rnext = rstd_in[row];
       uint32_t ph = 0;
       int k = 0;
       for (;; ++k) {
@@ -406,6 +412,7 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
         const int s = k % stages;
         mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
         slot[s] = row;
+        if constexpr (!kFwd) rslot[s] = rnext;
         mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
         uint8_t *st = smem + (size_t)s * stage_bytes;
         bulk_g2s(st, a + row * nvec, (uint32_t)row_bytes, &full[s]);
@@ -415,6 +422,7 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
         const int next = clc_query(clc_resp);
         if (next < 0) break;
         row = next;
+        if constexpr (!kFwd) rnext = rstd_in[row];
       }
       ++k;
       const int s = k % stages;
@@ -433,6 +441,8 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
     mbar_wait(&full[s], (uint32_t)(k / stages) & 1u);
     const int64_t row = slot[s];
     if (row < 0) break;
+    float r_row = 0.0f;
+    if constexpr (!kFwd) r_row = rslot[s];  // read before the stage is released
     const uint8_t *st = smem + (size_t)s * stage_bytes;
     uint4 ra[V], rb[V];
 #pragma unroll
@@ -500,7 +510,7 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
       }
       if (tid == 0) rstd_out[row] = r;
     } else {
-      const float r = rstd_in[row];
+      const float r = r_row;
       float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
@@ -560,7 +570,8 @@ static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
   int stages = (int)std::min<size_t>(4, (size_t)(96 * 1024) / stage);
   if (stages < 2) stages = 2;
-  const size_t tail = 16 + (2 * (size_t)stages + 1) * 8 + (size_t)stages * 8 + 64 * sizeof(float2);
+  const size_t tail = 16 + (2 * (size_t)stages + 1) * 8 + (size_t)stages * 8 + 64 * sizeof(float2) +
+                      (size_t)stages * sizeof(float);
   p.smem = (size_t)stages * stage + tail;
   if (p.smem > 227 * 1024) return p;
   p.ok = true;
