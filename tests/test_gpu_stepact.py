@@ -43,7 +43,7 @@ def _tables(k, rng):
 
 
 @pytest.mark.parametrize("k", [1, 2, 4])
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 @pytest.mark.parametrize("shape", [(1, 5), (7, 33), (64, 3072)])
 def test_stepact_vs_oracle(k, dtype, shape):
     rng = np.random.default_rng(k)
@@ -71,7 +71,7 @@ def test_stepact_bad_tables():
 
 
 @pytest.mark.parametrize("k", [1, 2, 4])
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 def test_stepact_paths_bitwise(k, dtype):
     """TMA pipeline path (aligned) == simple kernel path (misaligned codes)."""
     rng = np.random.default_rng(10 + k)
