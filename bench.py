@@ -206,6 +206,26 @@ def calibrate_rows(cfg, eps, target_s):
     return max(8, min(cfg["R"], int(rows * target_s / max(sec, 1e-4))))
 
 
+def measured_hbm_peak():
+    """HBM peak for the roofline: MEASURED_PEAKS.json (driver-written; the
+    burst copy figure, `hbm_gbs`, for kernels timed alone), else the fallback
+    the profiling guide states.  Tolerates a file without that key (any other
+    numeric `*hbm*gb*` entry, burst preferred over sustained)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if isinstance(d.get("hbm_gbs"), (int, float)):
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        keys = sorted((k for k, v in d.items() if isinstance(v, (int, float)) and "hbm" in k.lower()
+                       and "gb" in k.lower()), key=lambda k: ("sustain" in k.lower(), k))
+        if keys:
+            return float(d[keys[0]]), f"measured (MEASURED_PEAKS.json {keys[0]})"
+    except (OSError, ValueError, AttributeError):
+        pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -299,7 +319,7 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
     uf, ub = timeit(unfused_fwd), timeit(unfused_bwd)
     return {"shape": list(gate.shape), "fused_fwd_us": round(tf, 2), "fused_bwd_us": round(tb, 2),
             "fused_GB/s": round((bf + bb) / (tf + tb) / 1e3, 1),
-            "fused_frac": round((bf + bb) / (tf + tb) / 1e3 / 6536.0, 4),
+            "fused_frac": round((bf + bb) / (tf + tb) / 1e3 / measured_hbm_peak()[0], 4),
             "unfused_fwd_us": round(uf, 2), "unfused_bwd_us": round(ub, 2),
             "speedup_fwd_bwd": round((uf + ub) / (tf + tb), 3),
             "algorithmic_bytes": {"fwd": bf, "bwd": bb},
@@ -523,10 +543,7 @@ def main():
     max_ms = max(ms_all)
     value = aggregate(bytes_all, ms_all, args.steps)
 
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    if os.path.exists(peaks_path):
-        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    peak, peak_src = measured_hbm_peak()
 
     kern = {}
     for k in kernels:
