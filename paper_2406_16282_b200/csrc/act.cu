@@ -162,14 +162,25 @@ __device__ __forceinline__ uint32_t act_vec_op(const uint4 &v, uint32_t c_in, ui
   }
 }
 
-template <typename T, int A, bool kPrecise>
+// Forward pipeline shape (tools/sweep.py): 16-bit types 16 consumer warps x
+// 2 vectors x 4 stages; fp32 8 x 4 x 3 (C3 GELU fp32 67.6 -> 65.7 us,
+// profiles/r01/sweep24_fwd_shapes_c2_c3_c4.jsonl; no shape moves the
+// instruction-bound bf16 GELU at C2).
 #ifndef LMBP_FWD_W
 #define LMBP_FWD_W 16
 #define LMBP_FWD_U 2
 #define LMBP_FWD_S 4
 #endif
+#ifndef LMBP_FWD32_W
+#define LMBP_FWD32_W 8
+#define LMBP_FWD32_U 4
+#define LMBP_FWD32_S 3
+#endif
+template <typename T, int A, bool kPrecise>
 struct ActFwdOp {
-  static constexpr int W = LMBP_FWD_W, U = LMBP_FWD_U, S = LMBP_FWD_S, kIn = 1, kCodeIn = 0;
+  static constexpr bool k32 = sizeof(T) == 4;
+  static constexpr int W = k32 ? LMBP_FWD32_W : LMBP_FWD_W, U = k32 ? LMBP_FWD32_U : LMBP_FWD_U,
+                       S = k32 ? LMBP_FWD32_S : LMBP_FWD_S, kIn = 1, kCodeIn = 0;
   static constexpr int kCodeOut = Traits<T>::kVec / 4;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p) {
     return act_vec_op<T, A, kPrecise, true>(v[0], 0u, p.out[0], i);
