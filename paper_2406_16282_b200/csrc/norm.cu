@@ -731,6 +731,12 @@ __global__ void __launch_bounds__(256) norm_bwd_scalar(const T *dy, const T *y, 
 // ---------------------------------------------------------------------------
 // Launch configuration.
 // ---------------------------------------------------------------------------
+// Warp teams: the forward takes rows up to 8 vectors per lane (fp32 H = 768:
+// C3 18.4 -> 17.2 us, faster than a torch copy of its bytes), the backward up
+// to 4 (a 6-vector warp team measured slower there than the 64-thread CTA
+// team); profiles/r01/sweep25_norm_small_rows.jsonl.
+constexpr int kWarpVmaxFwd = 8, kWarpVmaxBwd = 4;
+
 struct RowPlan {
   bool vec;
   bool warp_team;
@@ -740,7 +746,7 @@ struct RowPlan {
 };
 
 template <typename T>
-static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void *c) {
+static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void *c, int warp_vmax) {
   constexpr int kVec = Traits<T>::kVec;
   RowPlan p{false, false, 0, 0, 0};
   const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)c % 16 == 0) &&
@@ -749,7 +755,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
   const int64_t nvec = cols / kVec;
   if (nvec > 8 * 512) return p;
   p.nvec = (int)nvec;
-  if (nvec <= 4 * 32) {  // one warp per row, up to 4 vectors per lane
+  if (nvec <= warp_vmax * 32) {  // one warp per row, up to warp_vmax vectors per lane
     p.warp_team = true;
     p.team = 32;
     p.V = (int)((nvec + 31) / 32);
@@ -760,7 +766,7 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
     p.team = (int)team;
     p.V = (int)((nvec + team - 1) / team);
   }
-  p.vec = p.V >= 1 && p.V <= (p.warp_team ? 4 : 8);
+  p.vec = p.V >= 1 && p.V <= (p.warp_team ? warp_vmax : 8);
   return p;
 }
 
@@ -783,12 +789,14 @@ static int occupancy_of(K kernel, int threads) {
 // Grid for the register-team kernels.  CTA teams (one row per CTA) launch one
 // CTA per row and let the hardware block scheduler balance the SMs (measured
 // C4 MS-RMSNorm fwd 22.4 -> 20.5 us, C3 MS-LN bwd 24.6 -> 22.5 us); warp teams
-// (8 short rows per CTA) keep a persistent grid, which measured faster there.
+// (8 short rows per CTA) of up to 4 vectors per lane keep a persistent grid,
+// which measured faster there (C2 bwd 14.4 vs 16.4 us); longer warp rows
+// (V > 4, the fp32 H = 768 forward) launch every CTA (C3 fwd 17.2 vs 18.4 us).
 template <typename K, typename... Args>
 static void launch_rows(K kernel, int64_t rows, int rows_per_block, int threads, cudaStream_t s, int occ,
-                        Args... args) {
+                        bool persistent, Args... args) {
   const int64_t want = (rows + rows_per_block - 1) / rows_per_block;
-  const int64_t cap = rows_per_block == 1 ? (int64_t)0x7fffffff : (int64_t)sm_count() * occ;
+  const int64_t cap = (rows_per_block == 1 || !persistent) ? (int64_t)0x7fffffff : (int64_t)sm_count() * occ;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
   kernel<<<grid, threads, 0, s>>>(args...);
 }
@@ -799,7 +807,7 @@ static void fwd_v(const RowPlan &p, const void *x, void *y, float *rstd, int64_t
   auto k = norm_fwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
   const int occ = occupancy_of(k, threads);
-  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, reinterpret_cast<const uint4 *>(x),
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, V <= 4, reinterpret_cast<const uint4 *>(x),
               reinterpret_cast<uint4 *>(y), rstd, rows, p.nvec, (int)cols, eps);
 }
 
@@ -809,14 +817,14 @@ static void bwd_v(const RowPlan &p, const void *dy, const void *y, const float *
   auto k = norm_bwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
   const int occ = occupancy_of(k, threads);
-  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, reinterpret_cast<const uint4 *>(dy),
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, true, reinterpret_cast<const uint4 *>(dy),
               reinterpret_cast<const uint4 *>(y), rstd, reinterpret_cast<uint4 *>(dx), rows, p.nvec, (int)cols);
 }
 
 template <typename T, int NORM>
 static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
                               cudaStream_t s) {
-  const RowPlan p = plan_rows<T>(cols, x, y, y);
+  const RowPlan p = plan_rows<T>(cols, x, y, y, kWarpVmaxFwd);
 #ifdef LMBP_ROW_TMA_FWD  // measured slower than the register teams for the forward (C4 24.6 vs 20.5 us)
   if (p.vec && rows > 0) {
     const RowTmaPlan rp = plan_row_tma(p.nvec, true);
@@ -836,15 +844,15 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
   }
   if (!p.vec) {
     auto k = norm_fwd_scalar<T, NORM>;
-    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
+    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), true, reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
                 rstd, rows, cols, eps);
     return cudaGetLastError();
   }
 #define LMBP_FWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= 4) {                                                                \
+    if constexpr (VV <= kWarpVmaxFwd) {                                                     \
       if (p.warp_team) {                                                                    \
-        fwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, x, y, rstd, rows, cols, eps, s);        \
+        fwd_v<T, NORM, (VV <= kWarpVmaxFwd ? VV : 1), true>(p, x, y, rstd, rows, cols, eps, s);        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \
@@ -862,7 +870,7 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
 template <typename T, int NORM>
 static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
                               int64_t cols, cudaStream_t s) {
-  const RowPlan p = plan_rows<T>(cols, dy, y, dx);
+  const RowPlan p = plan_rows<T>(cols, dy, y, dx, kWarpVmaxBwd);
 #ifndef LMBP_NO_ROW_TMA  // backward rows >= 256 vectors: row pipeline (C5 160 -> 147 us; C4 equal)
   if (p.vec && rows > 0) {
     const RowTmaPlan rp = plan_row_tma(p.nvec, false);
@@ -889,15 +897,15 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
   }
   if (!p.vec) {
     auto k = norm_bwd_scalar<T, NORM>;
-    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), reinterpret_cast<const T *>(dy),
+    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), true, reinterpret_cast<const T *>(dy),
                 reinterpret_cast<const T *>(y), rstd, reinterpret_cast<T *>(dx), rows, cols);
     return cudaGetLastError();
   }
 #define LMBP_BWD_CASE(VV)                                                                   \
   case VV:                                                                                  \
-    if constexpr (VV <= 4) {                                                                \
+    if constexpr (VV <= kWarpVmaxBwd) {                                                     \
       if (p.warp_team) {                                                                    \
-        bwd_v<T, NORM, (VV <= 4 ? VV : 4), true>(p, dy, y, rstd, dx, rows, cols, s);        \
+        bwd_v<T, NORM, (VV <= kWarpVmaxBwd ? VV : 1), true>(p, dy, y, rstd, dx, rows, cols, s);        \
         break;                                                                              \
       }                                                                                     \
     }                                                                                       \
