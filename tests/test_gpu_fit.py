@@ -155,3 +155,18 @@ def test_fitted_table_drives_stepact():
     xs = x.double().cpu().numpy().reshape(-1)
     want = np.array(lv)[np.searchsorted(np.array(c), xs, side="left")]
     assert np.array_equal(dx.cpu().numpy().reshape(-1), want.astype(np.float32))
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-3, 0.1])
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+def test_objective_other_tail_tolerances(act, eps):
+    """Other [A, B] (App. E's formulas at other eps): SiLU crosses the
+    tail-table threshold (>= 12 panels at 1e-6 / 1e-3, direct path at 0.1)."""
+    rng = np.random.default_rng(int(-np.log10(eps)) + 5 * (act == "silu"))
+    th = thetas(2, act, rng, 5)
+    A, B = ofit.tail_bounds(act, eps)
+    assert ops.fit_bounds(act, eps) == pytest.approx((A, B), rel=1e-15)
+    for obj in ("h", "dh"):
+        J = gfit.objective(th, act, k=2, objective=obj, eps=eps).cpu().numpy()
+        ref = np.array([ofit.objective(act, 2, t, OBJ[obj], eps=eps) for t in th])
+        assert np.all(np.abs(J - ref) <= 1e-10 * ref + 1e-13), (J, ref)

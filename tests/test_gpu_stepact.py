@@ -87,3 +87,31 @@ def test_stepact_paths_bitwise(k, dtype):
     torch.cuda.synchronize()
     assert torch.equal(c0, c1)
     assert st(y0).tobytes() == st(y1).tobytes() and st(dx0).tobytes() == st(dx1).tobytes()
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_stepact_k4_full_size_sampled(cfg):
+    """k = 4 at the BASELINE config's full activation size (TMA/CLC pipeline,
+    binary-search packed compares, shared-memory level table), sampled rows
+    against the oracle: codes bytewise, y within tolerance, dx bitwise."""
+    from test_gpu_parity import sample_rows
+    c = synth.CONFIGS[cfg]
+    R, F, dtype = c["R"], c["F"], c["dtype"]
+    thr = [-3.0 + 0.4 * i for i in range(15)]
+    lv = [(-1) ** i * i / 15 for i in range(16)]
+    x = synth.act_input(R, F, dtype, device=DEV)
+    dy = synth.grad_input(R, F, dtype, device=DEV)
+    y, codes = P.stepact_fwd(x, c["act"], 4, thr)
+    dx = P.stepact_bwd(dy, codes, 4, lv)
+    torch.cuda.synchronize()
+    rows = sample_rows(R)
+    idx = torch.tensor(rows, device=DEV)
+    assert F % 2 == 0
+    cb = codes.view(R, F // 2)[idx].cpu().numpy().reshape(-1)
+    xs = x[idx].cpu()
+    y_ref, c_ref = oracle.stepact_fwd(c["act"], 4, thr, dec(xs, dtype))
+    assert np.array_equal(cb, c_ref)
+    yr = y_ref.reshape(-1)
+    assert np.all(np.abs(dec(y[idx].cpu(), dtype).reshape(-1) - yr) <= RTOL[dtype] * np.abs(yr) + ATOL[dtype])
+    want = oracle.stepact_bwd_contract(4, lv, c_ref, st(dy[idx].cpu()), dtype)
+    assert np.array_equal(bits(st(dx[idx].cpu())), bits(want))
