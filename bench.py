@@ -170,11 +170,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the float64 oracle on a bounded row sample
 # ---------------------------------------------------------------------------
-def oracle_step_sample(cfg, rows, eps):
+def oracle_step_sample(cfg, rows, eps, threads=None):
     """One oracle pass of the four rows of 8(a) on `rows` rows; returns
-    (seconds, algorithmic bytes, threads)."""
+    (seconds, algorithmic bytes, threads).  threads=None: all usable cores."""
     import oracle
-    if oracle.DEFAULT_THREADS is None:      # all usable host cores, whatever OMP_NUM_THREADS says
+    if threads is not None:
+        oracle.DEFAULT_THREADS = int(threads)
+    elif oracle.DEFAULT_THREADS is None:    # all usable host cores, whatever OMP_NUM_THREADS says
         oracle.DEFAULT_THREADS = len(os.sched_getaffinity(0))
     dt = cfg["dtype"]
     x = synth.to_numpy_storage(synth.act_input(rows, cfg["F"], dt))
@@ -238,12 +240,19 @@ def cpu_model():
 
 
 def cpu_baseline(cfg, eps, target_s):
+    import oracle
     rows = calibrate_rows(cfg, eps, target_s)
     sec, nbytes, threads = oracle_step_sample(cfg, rows, eps)
+    # the same oracle on one core, on a proportionally smaller sample
+    rows1 = max(8, rows // max(1, threads))
+    sec1, nbytes1, _ = oracle_step_sample(cfg, rows1, eps, threads=1)
+    oracle.DEFAULT_THREADS = threads
     return {"value": round(nbytes / sec / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{rows} of {cfg['R']} rows of {cfg['desc']}: norm fwd+bwd and act fwd+bwd, float64 "
                       f"oracle incl. storage decode/encode, {sec:.2f} s",
-            "seconds": round(sec, 3), "rows": rows, "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
+            "seconds": round(sec, 3), "rows": rows, "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "single_core": {"value": round(nbytes1 / sec1 / 1e9, 4), "unit": "GB/s", "rows": rows1,
+                            "seconds": round(sec1, 3)}}
 
 
 def run_reference(args):
