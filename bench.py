@@ -384,10 +384,11 @@ PAPER_THETA = {  # P:L1062-1063 (GELU), P:L1139-1140 (SiLU), P:L1346-1347 (ReGEL
 def fitter_section(stream, cpu=True, chains=148 * 3 * 128, iters=1000, n_obj=148 * 3 * 128 * 4):
     """the offline coefficient fitter.  (1) batched
     objective throughput (J evaluations/s; one thread per theta, FP64-bound);
-    (2) a full simulated-annealing fit per (act, objective) of App. E / App. I
-    -- time, the J reached vs J at the paper's constants (both by the GPU
-    objective), the fitted constants; (3) the oracle's (QUADPACK) J/s on the
-    host for the cpu baseline."""
+    (2) a full fit per (act, objective) of App. E / App. I (variable-projection
+    annealing + LM refinement) -- time, the J reached vs J at the paper's
+    constants (both by the GPU objective), the fitted constants; (3) k = 1..4
+    fits (J falls with k); (4) the oracle's (QUADPACK) J/s on the host for the
+    cpu baseline."""
     from paper_2406_16282_b200 import fit as gfit
     from paper_2406_16282_b200 import ops
     out = {"chains": chains, "iters": iters}
@@ -409,7 +410,8 @@ def fitter_section(stream, cpu=True, chains=148 * 3 * 128, iters=1000, n_obj=148
     for act, obj in PAPER_THETA:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        best, cth, _ = ops.fit_anneal(act, objective=obj, chains=chains, iters=iters, stream=stream)
+        best, cth, _ = ops.fit_anneal(act, objective=obj, chains=chains, iters=iters, stream=stream,
+                                      projected=True)
         e1.record(stream)
         best2, _, _ = ops.fit_refine(cth, act, objective=obj, iters=40, stream=stream)
         e2 = torch.cuda.Event(enable_timing=True)
@@ -424,6 +426,18 @@ def fitter_section(stream, cpu=True, chains=148 * 3 * 128, iters=1000, n_obj=148
             "J_after_anneal": float(best[-1]),
             "J": b[-1], "J_paper": Jp, "J_over_paper": round(b[-1] / Jp, 6),
             "a": [round(v, 6) for v in b[:2]], "c": [round(v, 6) for v in b[2:5]]}
+    # k-bit fits (Eq. 14 with 2^k - 1 ReLUs; variable projection + LM)
+    kbit = {}
+    for act in ("gelu", "silu"):
+        kbit[act] = {}
+        for k, ch, it, ri in ((1, 4096, 300, 20), (2, 8192, 800, 40), (3, 8192, 2000, 20), (4, 4096, 4000, 8)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            f = gfit.fit(act, k=k, chains=ch, iters=it, refine_iters=ri)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            kbit[act][f"k{k}"] = {"J": f.J, "seconds": round(e0.elapsed_time(e1) / 1e3, 3)}
+    out["kbit_fits"] = kbit
     if cpu:
         from oracle import fit as ofit
         n, t0 = 0, time.perf_counter()

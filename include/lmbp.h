@@ -258,6 +258,19 @@ LMBP_API int lmbp_fit_anneal(int act, int objective, int k, double eps, const do
                              int64_t iters, uint64_t seed, double t0, double t1, double step0, double step1,
                              double *chain_theta, double *chain_J, double *best, void *stream);
 
+/* Variable-projection annealing: the same chains, but only the m thresholds
+ * anneal; for each proposal the weights are the exact least-squares optimum
+ * under sum w = 1 (Eq. 14's objective is quadratic in w for fixed c: a small
+ * (m+1)-dimensional linear solve), so the search space is m-dimensional and
+ * the weight directions' bad conditioning drops out (needed for k >= 3).
+ * init: as above (only its thresholds are used).  Steps scale with
+ * (B - A)/8.  Outputs as lmbp_fit_anneal, chain J re-evaluated by the direct
+ * quadrature.  When [A, B] spans more than 64 panels (eps below ~1e-27 for
+ * SiLU) every chain reports J = +inf (use lmbp_fit_anneal). */
+LMBP_API int lmbp_fit_anneal_vp(int act, int objective, int k, double eps, const double *init, int64_t chains,
+                                int64_t iters, uint64_t seed, double t0, double t1, double step0, double step1,
+                                double *chain_theta, double *chain_J, double *best, void *stream);
+
 /* Local refinement of n starting points (e.g. every annealing chain's best):
  * Levenberg-Marquardt on J with a central-difference gradient and Hessian
  * (steps 1e-4 x (1 for weights, (B - A)/8 for thresholds)), Cholesky solve

@@ -36,6 +36,8 @@ SIGNATURES = {
     "lmbp_fit_bounds": (_i32, [_i32, _f64, _p, _p]),
     "lmbp_fit_objective": (_i32, [_i32, _i32, _i32, _f64, _p, _p, _i64, _p]),
     "lmbp_fit_refine": (_i32, [_i32, _i32, _i32, _f64, _p, _i64, _i64, _p, _p, _p, _p]),
+    "lmbp_fit_anneal_vp": (_i32, [_i32, _i32, _i32, _f64, _p, _i64, _i64, _u64, _f64, _f64, _f64, _f64, _p, _p,
+                                  _p, _p]),
     "lmbp_fit_anneal": (_i32, [_i32, _i32, _i32, _f64, _p, _i64, _i64, _u64, _f64, _f64, _f64, _f64, _p, _p, _p,
                                _p]),
 }

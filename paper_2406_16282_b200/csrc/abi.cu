@@ -269,9 +269,9 @@ int lmbp_fit_objective(int act, int objective, int k, double eps, const double *
   return lmbp::status_of(lmbp::fit_objective(s, k, theta, J, n, static_cast<cudaStream_t>(stream)));
 }
 
-int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *init, int64_t chains, int64_t iters,
-                    uint64_t seed, double t0, double t1, double step0, double step1, double *chain_theta,
-                    double *chain_J, double *best, void *stream) {
+static int fit_anneal_entry(bool vp, int act, int objective, int k, double eps, const double *init, int64_t chains,
+                            int64_t iters, uint64_t seed, double t0, double t1, double step0, double step1,
+                            double *chain_theta, double *chain_J, double *best, void *stream) {
   lmbp::FitSpec s{};
   int st = lmbp::fit_spec(act, objective, k, eps, &s);
   if (st != LMBP_OK) return st;
@@ -280,8 +280,23 @@ int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *ini
     return LMBP_ERR_ARG;
   if (!chain_theta || !chain_J || !best) return LMBP_ERR_NULLPTR;
   lmbp::AnnealCfg a{chains, iters, seed, t0, t1, step0, step1};
-  return lmbp::status_of(
-      lmbp::fit_anneal(s, k, a, init, chain_theta, chain_J, best, static_cast<cudaStream_t>(stream)));
+  const cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  return lmbp::status_of(vp ? lmbp::fit_anneal_vp(s, k, a, init, chain_theta, chain_J, best, cs)
+                            : lmbp::fit_anneal(s, k, a, init, chain_theta, chain_J, best, cs));
+}
+
+int lmbp_fit_anneal(int act, int objective, int k, double eps, const double *init, int64_t chains, int64_t iters,
+                    uint64_t seed, double t0, double t1, double step0, double step1, double *chain_theta,
+                    double *chain_J, double *best, void *stream) {
+  return fit_anneal_entry(false, act, objective, k, eps, init, chains, iters, seed, t0, t1, step0, step1,
+                          chain_theta, chain_J, best, stream);
+}
+
+int lmbp_fit_anneal_vp(int act, int objective, int k, double eps, const double *init, int64_t chains, int64_t iters,
+                       uint64_t seed, double t0, double t1, double step0, double step1, double *chain_theta,
+                       double *chain_J, double *best, void *stream) {
+  return fit_anneal_entry(true, act, objective, k, eps, init, chains, iters, seed, t0, t1, step0, step1,
+                          chain_theta, chain_J, best, stream);
 }
 
 int lmbp_fit_refine(int act, int objective, int k, double eps, const double *theta, int64_t n, int64_t iters,

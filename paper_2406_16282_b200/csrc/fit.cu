@@ -399,6 +399,245 @@ __device__ __noinline__ double objective_call(const FitSpec &s, const double *th
   return objective_t<M>(s, th, T);
 }
 
+// ---------------------------------------------------------------------------
+// Variable projection.  For fixed thresholds c the objective is a quadratic
+// in the weights w under the linear constraint sum w = 1 (Eq. 14), so the
+// optimal weights are a small linear solve:
+//   J(w) = H0 - 2 b.w + w.G w,  G_ij = int r_i r_j,  b_i = int g r_i,
+//   G w = b - lambda 1,  1.w = 1   =>   J*(c) = H0 - b.w - lambda,
+// with r_i = ReLU(x - c_i), g = h (Eq. 15), or r_i = [x > c_i], g = h'
+// (Eq. 17), all over [A, B].  Annealing then moves only the m thresholds:
+// the search space halves and the ill-conditioned weight directions (an
+// outer ReLU's weight is ~-0.04) disappear from it, which is what lets
+// k >= 3 fits converge.  G has closed forms; b needs int_t^B h and
+// int_t^B x h (obj 0; obj 1: b_i = h(B) - h(c_i) exactly), tabulated per CTA
+// on the panel grid like the tail tables, plus one partial panel per kink.
+// J* carries the cancellation H0 - ... (H0 ~ 1.8e4 for SiLU vs J ~ 0.04: ~1e-11
+// relative), fine for the search; the reported J is re-evaluated directly.
+// ---------------------------------------------------------------------------
+struct VpTables {
+  int n;                                        // cells; 0 = interval too long for the table
+  double M0[kMaxCells + 1], M1[kMaxCells + 1];  // int_{x_i}^B h, int_{x_i}^B x h (obj 0)
+  double H0;                                    // int_A^B h^2 (obj 0) or h'^2 (obj 1)
+};
+
+// int g, int x g, int g^2 over [l, r] (g = h for obj 0, h' for obj 1), one panel.
+template <int ACT, int OBJ>
+__device__ __noinline__ void vp_cell_t(double l, double r, double *m0, double *m1, double *gg) {
+  const double mid = 0.5 * (l + r), half = 0.5 * (r - l);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < kGLN / 2; ++i) {
+    const double dx = half * gl_x(i);
+    const double x0 = mid - dx, x1 = mid + dx;
+    const double g0 = OBJ == 0 ? h_fn<ACT>(x0) : dh_fn<ACT>(x0);
+    const double g1 = OBJ == 0 ? h_fn<ACT>(x1) : dh_fn<ACT>(x1);
+    const double w = gl_w(i);
+    a0 = fma(w, g0 + g1, a0);
+    a1 = fma(w, fma(x0, g0, x1 * g1), a1);
+    a2 = fma(w, fma(g0, g0, g1 * g1), a2);
+  }
+  *m0 = a0 * half;
+  *m1 = a1 * half;
+  *gg = a2 * half;
+}
+
+__device__ __forceinline__ void vp_cell(const FitSpec &s, double l, double r, double *m0, double *m1, double *gg) {
+  if (s.act == kActGelu) {
+    if (s.obj == 0) vp_cell_t<kActGelu, 0>(l, r, m0, m1, gg);
+    else vp_cell_t<kActGelu, 1>(l, r, m0, m1, gg);
+  } else {
+    if (s.obj == 0) vp_cell_t<kActSilu, 0>(l, r, m0, m1, gg);
+    else vp_cell_t<kActSilu, 1>(l, r, m0, m1, gg);
+  }
+}
+
+__device__ __forceinline__ double vp_grid_x(const FitSpec &s, int n, int i) { return i >= n ? s.B : s.A + i * s.panel; }
+
+// Every thread of the block must call this (it synchronises the block).
+__device__ const VpTables *build_vp_tables(const FitSpec &s, VpTables &V, double *scratch /* >= kMaxCells */) {
+  const int n = (int)ceil((s.B - s.A) / s.panel);
+  if (threadIdx.x == 0) V.n = n <= kMaxCells ? n : 0;
+  __syncthreads();
+  if (V.n == 0) return nullptr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    vp_cell(s, vp_grid_x(s, n, i), vp_grid_x(s, n, i + 1), &V.M0[i], &V.M1[i], &scratch[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // suffix sums and the total, fixed order
+    V.M0[n] = V.M1[n] = 0.0;
+    double h0 = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+      V.M0[i] += V.M0[i + 1];
+      V.M1[i] += V.M1[i + 1];
+      h0 += scratch[i];
+    }
+    V.H0 = h0;
+  }
+  __syncthreads();
+  return &V;
+}
+
+// (int_t^B h, int_t^B x h) for t in [A, B].
+__device__ __forceinline__ void vp_moments(const FitSpec &s, const VpTables &V, double t, double *m0, double *m1) {
+  const int i = min(V.n - 1, max(0, (int)floor((t - s.A) / s.panel)));
+  double p0, p1, p2;
+  vp_cell(s, t, vp_grid_x(s, V.n, i + 1), &p0, &p1, &p2);
+  *m0 = V.M0[i + 1] + p0;
+  *m1 = V.M1[i + 1] + p1;
+}
+
+__device__ __forceinline__ double h_any(int act, double x) {
+  return act == kActGelu ? h_fn<kActGelu>(x) : h_fn<kActSilu>(x);
+}
+
+// J*(c) and the optimal weights w (sum w = 1).  +inf if the normal equations
+// are singular (e.g. several kinks beyond B).
+template <int M>
+__device__ double vp_objective(const FitSpec &s, const VpTables &V, const double *c, double *w) {
+  double cc[M], b[M], G[M * M];
+  for (int i = 0; i < M; ++i) {
+    cc[i] = fmin(fmax(c[i], s.A), s.B);
+    if (s.obj == 0) {
+      double m0, m1;
+      vp_moments(s, V, cc[i], &m0, &m1);
+      b[i] = fma(-c[i], m0, m1);                    // int_{cc}^B h (x - c)
+    } else {
+      b[i] = h_any(s.act, s.B) - h_any(s.act, cc[i]);  // int_{cc}^B h'
+    }
+  }
+  for (int i = 0; i < M; ++i) {
+    for (int j = 0; j <= i; ++j) {
+      const double m = fmax(cc[i], cc[j]);
+      double g;
+      if (s.obj == 0) {  // int_m^B (x - c_i)(x - c_j), u = x - c_i
+        const double u0 = m - c[i], u1 = s.B - c[i], d = c[i] - c[j];
+        g = (u1 * u1 * u1 - u0 * u0 * u0) / 3.0 + d * (u1 * u1 - u0 * u0) * 0.5;
+      } else {
+        g = s.B - m;
+      }
+      G[i * M + j] = G[j * M + i] = g;
+    }
+  }
+  // Cholesky with a relative ridge, two right-hand sides (b and 1).
+  double L[M * M];
+  for (int i = 0; i < M; ++i) {
+    for (int j = 0; j <= i; ++j) {
+      double v = G[i * M + j] + (i == j ? 1e-13 * (fabs(G[i * M + i]) + 1.0) : 0.0);
+      for (int q = 0; q < j; ++q) v -= L[i * M + q] * L[j * M + q];
+      if (i == j) {
+        if (!(v > 0.0)) return INFINITY;
+        L[i * M + i] = sqrt(v);
+      } else {
+        L[i * M + j] = v / L[j * M + j];
+      }
+    }
+  }
+  double y[M], z[M];
+  for (int i = 0; i < M; ++i) {
+    double vy = b[i], vz = 1.0;
+    for (int q = 0; q < i; ++q) {
+      vy -= L[i * M + q] * y[q];
+      vz -= L[i * M + q] * z[q];
+    }
+    y[i] = vy / L[i * M + i];
+    z[i] = vz / L[i * M + i];
+  }
+  for (int i = M - 1; i >= 0; --i) {
+    double vy = y[i], vz = z[i];
+    for (int q = i + 1; q < M; ++q) {
+      vy -= L[q * M + i] * y[q];
+      vz -= L[q * M + i] * z[q];
+    }
+    y[i] = vy / L[i * M + i];
+    z[i] = vz / L[i * M + i];
+  }
+  double sy = 0.0, sz = 0.0;
+  for (int i = 0; i < M; ++i) {
+    sy += y[i];
+    sz += z[i];
+  }
+  const double lam = (sy - 1.0) / sz;
+  double bw = 0.0;
+  for (int i = 0; i < M; ++i) {
+    w[i] = y[i] - lam * z[i];
+    bw += b[i] * w[i];
+  }
+  const double J = V.H0 - bw - lam;
+  return isfinite(J) ? fmax(J, 0.0) : INFINITY;
+}
+
+template <int M>
+__device__ __noinline__ double vp_call(const FitSpec &s, const VpTables &V, const double *c, double *w) {
+  return vp_objective<M>(s, V, c, w);
+}
+
+// Annealing over the thresholds only, weights by variable projection.  Same
+// proposal / acceptance / step adaptation as fit_anneal_k; the chain's best
+// (w*, c) is written in canonical form with its J re-evaluated by the direct
+// quadrature (objective_t).  Intervals too long for the table: J = +inf.
+template <int M>
+__global__ void __launch_bounds__(128) fit_anneal_vp_k(FitSpec s, AnnealCfg a, const double *init,
+                                                        double *chain_theta, double *chain_J) {
+  constexpr int P = 2 * M - 1;
+  __shared__ VpTables vt;
+  __shared__ double scratch[kMaxCells];
+  const VpTables *V = build_vp_tables(s, vt, scratch);
+  const int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= a.chains) return;
+  if (!V) {
+    for (int i = 0; i < P; ++i) chain_theta[ch * P + i] = 0.0;
+    chain_J[ch] = INFINITY;
+    return;
+  }
+  const double cscale = (s.B - s.A) * 0.125;
+  double c[M], w[M], bc[M], bw[M], sig[M], pc[M], pw[M];
+  uint64_t ctr = 0;
+  for (int i = 0; i < M; ++i) {
+    c[i] = init ? init[M - 1 + i] : s.A * 0.5 + (s.B - s.A) * 0.5 * u01(a.seed, ch, ctr++);
+    sig[i] = a.step0 * cscale;
+  }
+  double J = vp_call<M>(s, *V, c, w);
+  double bestJ = J;
+  for (int i = 0; i < M; ++i) {
+    bc[i] = c[i];
+    bw[i] = w[i];
+  }
+  ctr = 1ull << 40;
+  const double lt = log(a.t1 / a.t0);
+  for (int64_t it = 0; it < a.iters; ++it) {
+    const double frac = a.iters > 1 ? (double)it / (double)(a.iters - 1) : 1.0;
+    const double temp = a.t0 * exp(lt * frac);
+    const int j = (int)(it % M);
+    const double g = gauss(a.seed, ch, ctr);
+    const double u = u01(a.seed, ch, (1ull << 62) + ctr);
+    ctr += 1;
+    for (int i = 0; i < M; ++i) pc[i] = c[i] + (i == j ? sig[i] * g : 0.0);
+    const double Jp = vp_call<M>(s, *V, pc, pw);
+    const bool acc = Jp <= J || u < exp((J - Jp) / (temp * J));
+    sig[j] = fmin(fmax(sig[j] * (acc ? 1.25 : 0.92), a.step1 * cscale), 4.0 * a.step0 * cscale);
+    if (acc) {
+      J = Jp;
+      for (int i = 0; i < M; ++i) {
+        c[i] = pc[i];
+        w[i] = pw[i];
+      }
+      if (J < bestJ) {
+        bestJ = J;
+        for (int i = 0; i < M; ++i) {
+          bc[i] = c[i];
+          bw[i] = w[i];
+        }
+      }
+    }
+  }
+  double th[P], out[P];
+  for (int i = 0; i < M - 1; ++i) th[i] = bw[i];
+  for (int i = 0; i < M; ++i) th[M - 1 + i] = bc[i];
+  canonical<M>(th, out);
+  for (int i = 0; i < P; ++i) chain_theta[ch * P + i] = out[i];
+  chain_J[ch] = objective_call<M>(s, out, nullptr);
+}
+
 template <int P>
 __device__ bool cholesky_solve(const double *H, const double *g, double lam, double *d) {
   double L[P * P];
@@ -546,6 +785,18 @@ cudaError_t anneal_m(const FitSpec &s, const AnnealCfg &a, const double *init, d
 }
 
 template <int M>
+cudaError_t anneal_vp_m(const FitSpec &s, const AnnealCfg &a, const double *init, double *chain_theta,
+                        double *chain_J, double *best, cudaStream_t st) {
+  const int64_t blocks = (a.chains + 127) / 128;
+  if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+  fit_anneal_vp_k<M><<<(int)blocks, 128, 0, st>>>(s, a, init, chain_theta, chain_J);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  fit_best_k<<<1, 1024, 0, st>>>(chain_theta, chain_J, a.chains, 2 * M - 1, best);
+  return cudaGetLastError();
+}
+
+template <int M>
 cudaError_t refine_m(const FitSpec &s, const double *in, int64_t n, int64_t iters, double *out, double *Jout,
                      double *best, cudaStream_t st) {
   const int64_t blocks = (n + 127) / 128;
@@ -558,6 +809,16 @@ cudaError_t refine_m(const FitSpec &s, const double *in, int64_t n, int64_t iter
 }
 
 }  // namespace
+
+cudaError_t fit_anneal_vp(const FitSpec &s, int k, const AnnealCfg &a, const double *init, double *chain_theta,
+                          double *chain_J, double *best, cudaStream_t st) {
+  switch (k) {
+    case 1: return anneal_vp_m<1>(s, a, init, chain_theta, chain_J, best, st);
+    case 2: return anneal_vp_m<3>(s, a, init, chain_theta, chain_J, best, st);
+    case 3: return anneal_vp_m<7>(s, a, init, chain_theta, chain_J, best, st);
+    default: return anneal_vp_m<15>(s, a, init, chain_theta, chain_J, best, st);
+  }
+}
 
 cudaError_t fit_refine(const FitSpec &s, int k, const double *in, int64_t n, int64_t iters, double *out,
                        double *Jout, double *best, cudaStream_t st) {

@@ -44,6 +44,8 @@ struct AnnealCfg {
 cudaError_t fit_objective(const FitSpec &s, int k, const double *theta, double *J, int64_t n, cudaStream_t st);
 cudaError_t fit_anneal(const FitSpec &s, int k, const AnnealCfg &a, const double *init, double *chain_theta,
                        double *chain_J, double *best, cudaStream_t st);
+cudaError_t fit_anneal_vp(const FitSpec &s, int k, const AnnealCfg &a, const double *init, double *chain_theta,
+                          double *chain_J, double *best, cudaStream_t st);
 cudaError_t fit_refine(const FitSpec &s, int k, const double *in, int64_t n, int64_t iters, double *out,
                        double *Jout, double *best, cudaStream_t st);
 

@@ -286,10 +286,11 @@ def fit_objective(theta, act: str, k: int = 2, objective: str = "h", eps: float 
 
 def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, chains: int = 148 * 128,
                iters: int = 3000, seed: int = 2406, t0: float = 0.1, t1: float = 1e-9, step0: float = 0.3,
-               step1: float = 1e-9, init=None, device="cuda", stream=None):
+               step1: float = 1e-9, init=None, device="cuda", stream=None, projected: bool = False):
     """Simulated annealing on the GPU, one chain per thread.  Returns
     (best [P + 1] = theta then J, chain_theta [chains, P], chain_J [chains]),
-    all CUDA float64 tensors."""
+    all CUDA float64 tensors.  projected=True: lmbp_fit_anneal_vp (anneal
+    the thresholds, weights by least squares)."""
     P = fit_n_params(k)
     if init is not None:
         _need(init, "init")
@@ -298,7 +299,8 @@ def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, ch
     chain_theta = torch.empty(chains, P, dtype=torch.float64, device=device)
     chain_J = torch.empty(chains, dtype=torch.float64, device=device)
     best = torch.empty(P + 1, dtype=torch.float64, device=device)
-    check("lmbp_fit_anneal", lib().lmbp_fit_anneal(
+    fn = "lmbp_fit_anneal_vp" if projected else "lmbp_fit_anneal"
+    check(fn, getattr(lib(), fn)(
         _ACT[act], _OBJ[objective], int(k), float(eps), None if init is None else init.data_ptr(), int(chains),
         int(iters), int(seed) & (2 ** 64 - 1), float(t0), float(t1), float(step0), float(step1),
         chain_theta.data_ptr(), chain_J.data_ptr(), best.data_ptr(), _stream(stream)))

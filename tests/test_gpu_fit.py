@@ -120,8 +120,52 @@ def test_anneal_k1_matches_oracle_minimum(act, obj):
 
 
 def test_anneal_more_bits_fit_better():
-    J = [gfit.fit("gelu", k=k, chains=2048, iters=600 * (2 * ((1 << k) - 1) - 1), seed=5).J for k in (1, 2, 3)]
+    J = [gfit.fit("gelu", k=k, chains=2048, iters=600 * (2 * ((1 << k) - 1) - 1), seed=5, projected=False).J
+         for k in (1, 2, 3)]
     assert J[0] > J[1] > J[2] > 0
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+@pytest.mark.parametrize("obj", ["h", "dh"])
+def test_projected_anneal_same_k2_optimum(act, obj):
+    """Variable projection (thresholds annealed, weights by least squares)
+    lands on the same k = 2 optimum as annealing all five parameters."""
+    fp = gfit.fit(act, k=2, objective=obj, chains=2048, iters=800, seed=9, projected=True)
+    fa = gfit.fit(act, k=2, objective=obj, chains=4096, iters=2000, seed=9, projected=False)
+    assert fp.J == pytest.approx(fa.J, rel=1e-9)
+    assert np.allclose(fp.a + fp.c, fa.a + fa.c, atol=1e-4)
+    J_ref = ofit.objective(act, 2, np.array(fp.a + fp.c), OBJ[obj])
+    assert fp.J == pytest.approx(J_ref, rel=1e-9)
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+def test_projected_weights_are_least_squares_optimal(act):
+    """For the thresholds it returns, the projected search's weights minimise
+    the ORACLE's objective under sum w = 1: moving weight between any two
+    ReLUs (the constraint-preserving directions) raises J."""
+    best, th, J = ops.fit_anneal(act, k=2, chains=512, iters=300, seed=4, projected=True)
+    t = best[:5].cpu().numpy()
+    J0 = ofit.objective(act, 2, t)
+    for d in ([1e-4, 0.0], [0.0, 1e-4], [1e-4, -1e-4]):     # a1, a2 (w3 = 1 - a1 - a2 absorbs)
+        for sgn in (1, -1):
+            tp = t.copy()
+            tp[:2] += sgn * np.array(d)
+            assert ofit.objective(act, 2, tp) > J0
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+def test_projected_kbit_fits(act):
+    """k = 1..4 with variable projection: J* falls strictly with k, each
+    fit's J is the oracle's J of its point, and the k = 4 fit beats the
+    all-parameter annealing (which stalls with ReLUs parked in a tail)."""
+    Js, f = [], None
+    for k, chains, iters in ((1, 1024, 300), (2, 2048, 800), (3, 4096, 2000), (4, 4096, 4000)):
+        f = gfit.fit(act, k=k, chains=chains, iters=iters, seed=11, refine_iters=8 if k == 4 else 20)
+        Js.append(f.J)
+        assert f.J == pytest.approx(ofit.objective(act, k, np.array(f.a + f.c)), rel=1e-8)
+    assert Js[0] > Js[1] > Js[2] > Js[3] > 0, Js
+    plain = gfit.fit(act, k=4, chains=4096, iters=4000, seed=11, refine_iters=8, projected=False)
+    assert Js[3] < plain.J
 
 
 def test_anneal_deterministic_and_launch_independent():
