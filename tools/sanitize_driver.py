@@ -39,5 +39,7 @@ for act in ("gelu", "silu"):
         P.ops.fit_objective(th, act, k=k, objective="dh")
     best, cth, cj = P.ops.fit_anneal(act, chains=150, iters=20)
     P.ops.fit_refine(cth, act, iters=2)
+    for k in (1, 2, 4):
+        P.ops.fit_anneal(act, k=k, chains=70, iters=10, projected=True)
 torch.cuda.synchronize()
 print("sanitize driver ok")
