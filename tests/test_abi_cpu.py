@@ -170,3 +170,38 @@ def test_fit_bounds_and_validation_without_device_work():
             kw = dict(args); kw[key] = bad
             assert ann(**kw) == S.LMBP_ERR_ARG
     assert ann(ptr=None) == S.LMBP_ERR_NULLPTR
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """The boundary is a C ABI: include/lmbp.h compiles as strict C11, a C
+    program links against liblmbp.so and gets the documented host-side
+    results (no device work: sizes, status strings, fitter bounds and a
+    validation error)."""
+    import subprocess
+    src = tmp_path / "abi_probe.c"
+    src.write_text(r'''
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include "lmbp.h"
+int main(void) {
+  double A = 0.0, B = 0.0;
+  float thr[3], lvl[4];
+  if (lmbp_codes_bytes(5) != 2 || lmbp_codes_bytes_k(5, 4) != 3) return 1;
+  if (strncmp(lmbp_version(), "lmbp", 4) != 0) return 2;
+  if (lmbp_fit_bounds(LMBP_GELU, 1e-8, &A, &B) != LMBP_OK || fabs(B - sqrt(-2.0 * log(1e-8))) > 1e-12 || A != -B)
+    return 3;
+  if (lmbp_step_table(LMBP_SILU, thr, lvl) != LMBP_OK || lvl[3] != 1.0f) return 4;
+  if (regelu2_fwd(NULL, NULL, NULL, 4, 8, 9, NULL) != LMBP_ERR_DTYPE) return 5;
+  if (msln_fwd(NULL, NULL, NULL, 4, 8, -1.0f, LMBP_F32, NULL) != LMBP_ERR_EPS) return 6;
+  printf("%s\n", lmbp_status_string(LMBP_ERR_SHAPE));
+  return 0;
+}
+''')
+    lib_dir = os.path.dirname(_lib.LIB)
+    exe = tmp_path / "abi_probe"
+    subprocess.run(["gcc", "-std=c11", "-pedantic", "-Wall", "-Wextra", "-Werror", f"-I{os.path.join(ROOT, 'include')}",
+                    str(src), "-o", str(exe), f"-L{lib_dir}", "-llmbp", f"-Wl,-rpath,{lib_dir}", "-lm"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    assert r.stdout.startswith("LMBP_ERR_SHAPE")
