@@ -118,7 +118,7 @@ def bytes_saved(cfg, R):
 # ---------------------------------------------------------------------------
 class ClockSampler:
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.mem, self.reasons, self.max_mhz = [], [], set(), None
         self._stop = threading.Event()
         self._t = None
         try:
@@ -134,6 +134,7 @@ class ClockSampler:
     def _sample(self):
         nv = self.nv
         self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        self.mem.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM))
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                  "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
@@ -164,7 +165,7 @@ class ClockSampler:
                 pass
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "mem_mhz": statistics.median(self.mem) if self.mem else None}
 
 
 # ---------------------------------------------------------------------------
