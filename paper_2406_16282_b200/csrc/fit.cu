@@ -21,6 +21,13 @@
 // rule errs by ~1e-26 relative; GELU is entire.  The objective is ALU (FP64)
 // bound; nothing is read from memory but the parameters.
 //
+// Kernels: fit_objective_k (batched J), fit_anneal_k (all 2m - 1 parameters
+// annealed), fit_anneal_vp_k (thresholds annealed, weights by the
+// constrained least-squares solve -- variable projection), fit_refine_k
+// (Levenberg-Marquardt from each chain's best), fit_best_k (deterministic
+// arg-min).  Per-CTA shared-memory tables of the theta-independent integrals
+// (tails; moments for the projection) replace most panels on long intervals.
+//
 // The oracle (oracle/fit.py) evaluates the same integral with QUADPACK; the
 // two share nothing.
 #include <cmath>
