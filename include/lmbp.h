@@ -220,7 +220,9 @@ LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint
  *   (Eq. 17).  k: 1..4.  eps: the tail tolerance that fixes [A, B]
  *   (lmbp_fit_bounds; the paper uses 1e-8).
  * Arithmetic: binary64 throughout; the integral is a composite 16-point
- *   Gauss-Legendre rule on panels of length <= 2 between the sorted kinks.
+ *   Gauss-Legendre rule on panels of length <= 2 between the sorted kinks
+ *   (on intervals of >= 12 panels the theta-independent outer pieces come
+ *   from per-block prefix tables plus one partial panel each).
  * Errors: act / objective unknown -> LMBP_ERR_KIND; k outside 1..4 or
  *   n < 0 -> LMBP_ERR_SHAPE; eps not in (0, 1) -> LMBP_ERR_EPS; NULL pointer
  *   with work to do -> LMBP_ERR_NULLPTR; bad annealing schedule (chains < 1,
