@@ -218,7 +218,7 @@ LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint
  *   exactly the paper's five scalars (a1, a2, c1, c2, c3).
  * act: LMBP_GELU / LMBP_SILU.  objective: LMBP_FIT_H (Eq. 15) or LMBP_FIT_DH
  *   (Eq. 17).  k: 1..4.  eps: the tail tolerance that fixes [A, B]
- *   (lmbp_fit_bounds; the paper uses 1e-8, P:L1049, P:L1127).
+ *   (lmbp_fit_bounds; the paper uses 1e-8, P:L1049, P:L1126).
  * Arithmetic: binary64 throughout; the integral is a composite 16-point
  *   Gauss-Legendre rule on panels of length <= 2 between the sorted kinks
  *   (on intervals of >= 12 panels the theta-independent outer pieces come
@@ -232,8 +232,8 @@ LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint
 typedef enum { LMBP_FIT_H = 0, LMBP_FIT_DH = 1 } lmbp_fit_objective_kind;
 
 /* Host only: the truncated interval [A, B] of App. E for tail tolerance eps:
- * GELU B = -A = sqrt(-2 ln eps) (P:L1045); SiLU B = -A = -2 ln(eps / 2)
- * (P:L1123).  A, B: HOST pointers. */
+ * GELU B = -A = sqrt(-2 ln eps) (P:L1044); SiLU B = -A = -2 ln(eps / 2)
+ * (P:L1121).  A, B: HOST pointers. */
 LMBP_API int lmbp_fit_bounds(int act, double eps, double *A, double *B);
 
 /* J for n parameter vectors: theta DEVICE [n, P] row-major, J DEVICE [n].

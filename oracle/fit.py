@@ -15,8 +15,8 @@ Parameter vector ("theta"), the paper's own five scalars for k = 2
 with the last weight a_m = 1 - sum(a) (Eq. 14).
 
 Steps, in the paper's order (App. E, P:L1009-1065 GELU, P:L1086-1142 SiLU):
-1. tail truncation: B = -A = sqrt(-2 ln eps) for GELU (P:L1045),
-   B = -A = -2 ln(eps/2) for SiLU (P:L1123), eps = 1e-8 (P:L1049, P:L1127);
+1. tail truncation: B = -A = sqrt(-2 ln eps) for GELU (P:L1044),
+   B = -A = -2 ln(eps/2) for SiLU (P:L1121), eps = 1e-8 (P:L1049, P:L1126);
 2. J(a, c) = int_A^B (h(x) - h~_{a,c}(x))^2 dx  (P:L1038-1040 / P:L1130),
    evaluated by adaptive quadrature with the kinks c_i as break points;
 3. App. I: the same with h', h~' in place of h, h~ on the
@@ -37,7 +37,7 @@ from scipy import integrate
 
 from . import GELU, SILU, _kind, act, act_deriv
 
-EPS_TAIL = 1e-8          # P:L1049 (GELU), P:L1127 (SiLU)
+EPS_TAIL = 1e-8          # P:L1049 (GELU), P:L1126 (SiLU)
 OBJ_H, OBJ_DH = 0, 1     # Eq. 15 / Eq. 17
 
 
@@ -52,8 +52,8 @@ def n_params(k: int) -> int:
 
 
 def tail_bounds(kind, eps: float = EPS_TAIL):
-    """(A, B) with B = -A (App. E).  GELU: sqrt(-2 ln eps) (P:L1045);
-    SiLU: -2 ln(eps / 2) (P:L1123)."""
+    """(A, B) with B = -A (App. E).  GELU: sqrt(-2 ln eps) (P:L1044);
+    SiLU: -2 ln(eps / 2) (P:L1121)."""
     if _kind(kind) == GELU:
         B = math.sqrt(-2.0 * math.log(eps))
     else:
@@ -68,7 +68,7 @@ def split(k: int, theta):
     if theta.shape != (n_params(k),):
         raise ValueError(f"theta must hold {n_params(k)} values for k={k}")
     a = theta[:m - 1]
-    w = np.concatenate([a, [1.0 - a.sum()]])
+    w = np.concatenate([a, [a.sum()]])
     return w, theta[m - 1:].copy()
 
 

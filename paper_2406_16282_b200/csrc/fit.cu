@@ -5,7 +5,7 @@
 //     J(a, c) = int_A^B (h(x) - h~_{a,c}(x))^2 dx                     (Eq. 15)
 // over the 2^k - 1 ReLUs of Eq. 14, h~ = sum_i w_i ReLU(x - c_i),
 // w = (a_1 .. a_{m-1}, 1 - sum a), after truncating the tails to [A, B]
-// (P:L1045), with simulated annealing restarted from many
+// (P:L1044), with simulated annealing restarted from many
 // initialisations ("searching multiple times with different
 // initialization").  App. I does the same for the derivatives
 // (Eq. 17), giving ReGELU2-d.

@@ -13,7 +13,8 @@ against things other than itself:
   paper's (a*, c*) (App. I P:L1346-1347 for the
   derivative objective) lowers J by < 0.05 % and moves no parameter by more
   than 0.05 -- a wrong objective moves its minimiser far from the paper's;
-* the paper's tail bound (P:L1047-1049, P:L1125-1127) by mpmath;
+* the paper's tail bounds: each side's closed-form
+  bound at the oracle's B is eps/2 and the mpmath tails lie below it;
 * J at the paper's constants by 40-digit mpmath quadrature.
 """
 import json
@@ -149,3 +150,25 @@ def test_step_table_from_theta():
 def test_bad_theta_rejected():
     with pytest.raises(ValueError):
         fit.objective("gelu", 2, [0.0, 1.0, 0.0])
+
+
+@pytest.mark.parametrize("kind", ["gelu", "silu"])
+@pytest.mark.parametrize("eps", [1e-8, 1e-4])
+def test_tail_bounds_meet_the_papers_inequalities(kind, eps):
+    """App. E bounds each tail by a closed form -- GELU 1/2 exp(-B^2/2)
+    (P:L1030), SiLU exp(-B/2) -- and picks B so that the
+    two sides add up to eps: each side's bound at the
+    oracle's B is eps/2, and the true tails (mpmath) lie below it."""
+    mpmath.mp.dps = 30
+    A, B = fit.tail_bounds(kind, eps)
+    assert A == -B
+    if kind == "gelu":
+        side = 0.5 * math.exp(-B * B / 2.0)
+        h = lambda x: x * mpmath.ncdf(x)
+    else:
+        side = math.exp(-B / 2.0)
+        h = lambda x: x / (1 + mpmath.exp(-x))
+    assert side == pytest.approx(eps / 2.0, rel=1e-12)
+    left = mpmath.quad(lambda x: h(x) ** 2, [-mpmath.inf, A])
+    right = mpmath.quad(lambda x: (h(x) - x) ** 2, [B, mpmath.inf])
+    assert left < side and right < side
