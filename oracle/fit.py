@@ -68,7 +68,7 @@ def split(k: int, theta):
     if theta.shape != (n_params(k),):
         raise ValueError(f"theta must hold {n_params(k)} values for k={k}")
     a = theta[:m - 1]
-    w = np.concatenate([a, [a.sum()]])
+    w = np.concatenate([a, [1.0 - a.sum()]])
     return w, theta[m - 1:].copy()
 
 
