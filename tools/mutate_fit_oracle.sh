@@ -4,7 +4,11 @@
 # Every mutation below must make at least one pin fail.
 cd "$(dirname "$0")/.."
 mkdir -p /tmp/mut
+# never start from (or leave behind) a mutant: the file must match git HEAD,
+# and it is restored on any exit (an interrupted run once left one behind)
+git diff --quiet HEAD -- oracle/fit.py || { echo "oracle/fit.py differs from HEAD; refusing"; exit 1; }
 cp oracle/fit.py /tmp/mut/fit_orig.py
+trap 'cp /tmp/mut/fit_orig.py oracle/fit.py' EXIT
 run() {
   python - "$1" "$2" <<'PY'
 import sys
