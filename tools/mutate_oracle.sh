@@ -3,8 +3,11 @@
 # run tests/test_oracle_pins.py, restore.  Every mutation listed in DESIGN.md
 # ("Oracle pins") must make at least one pin fail.
 # usage: run.sh 'sed-expr'
-cd /root/repo
+cd "$(dirname "$0")/.."
+mkdir -p /tmp/mut
+git diff --quiet HEAD -- oracle/oracle.c || { echo "oracle/oracle.c differs from HEAD; refusing"; exit 1; }
 cp oracle/oracle.c /tmp/mut/orig.c
+trap 'cp /tmp/mut/orig.c oracle/oracle.c; rm -f oracle/liboracle.so' EXIT
 sed -i "$1" oracle/oracle.c
 if cmp -s oracle/oracle.c /tmp/mut/orig.c; then echo "NO CHANGE: $1"; fi
 rm -f oracle/liboracle.so
