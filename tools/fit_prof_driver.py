@@ -1,5 +1,6 @@
 """Driver for ncu captures of the coefficient-fitter kernels: one batched
-objective launch per activation, one annealing launch, one refinement launch."""
+objective launch per activation, one annealing launch, one refinement launch,
+one variable-projection annealing launch."""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import torch
@@ -13,5 +14,6 @@ for act in ("gelu", "silu"):
     ops.fit_objective(batch, act)
 best, cth, cj = ops.fit_anneal("silu", chains=148 * 3 * 128, iters=200)
 ops.fit_refine(cth, "silu", iters=5)
+ops.fit_anneal("silu", chains=148 * 3 * 128, iters=200, projected=True)
 torch.cuda.synchronize()
 print("ok")
