@@ -677,6 +677,7 @@ def main():
             "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_gpu": R, "act_cols": F,
                        "norm_cols": H, "act": cfg["act"], "norm": cfg["norm"], "eps": args.eps,
                        "step": "norm_fwd, act_fwd, act_bwd, norm_bwd",
+                       "arithmetic": f"binary32 in registers, {dt} storage (codes: 2-bit packed uint8)",
                        "l2": "flushed before every kernel by reading a 2x L2 buffer (L2 left clean), outside the CUDA events",
                        "parallelism": f"dp{world} (rows per rank, no data-path collective)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
