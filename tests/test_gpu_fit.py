@@ -214,3 +214,36 @@ def test_objective_other_tail_tolerances(act, eps):
         J = gfit.objective(th, act, k=2, objective=obj, eps=eps).cpu().numpy()
         ref = np.array([ofit.objective(act, 2, t, OBJ[obj], eps=eps) for t in th])
         assert np.all(np.abs(J - ref) <= 1e-10 * ref + 1e-13), (J, ref)
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+@pytest.mark.parametrize("obj", ["h", "dh"])
+def test_projection_weights_vs_kkt_solve(act, obj):
+    """lmbp_fit_anneal_vp with zero steps returns, for the thresholds it is
+    given, the weights of the constrained least-squares problem.  Reference:
+    the KKT system [[G, 1], [1^T, 0]] [w; lam] = [b; 1] with G_ij = int r_i r_j
+    and b_i = int g r_i evaluated by QUADPACK (g = h, r = ReLU(x - c); or
+    g = h', r = [x > c]) on the oracle's [A, B]."""
+    from scipy import integrate
+    import oracle
+    rng = np.random.default_rng(21 + (act == "silu") + 2 * (obj == "dh"))
+    A, B = ofit.tail_bounds(act)
+    for _ in range(3):
+        c = np.sort(rng.uniform(0.5 * A, 0.5 * B, 3))
+        init = torch.tensor([0.3, 0.3, *c], dtype=torch.float64, device=DEV)
+        best, th, J = ops.fit_anneal(act, objective=obj, chains=1, iters=0, init=init, projected=True)
+        t = th[0].cpu().numpy()
+        if obj == "h":
+            r = [lambda x, ci=ci: max(x - ci, 0.0) for ci in c]
+            g = lambda x: oracle.act(act, x)
+        else:
+            r = [lambda x, ci=ci: 1.0 if x > ci else 0.0 for ci in c]
+            g = lambda x: oracle.act_deriv(act, x)
+        q = lambda f: integrate.quad(f, A, B, points=list(c), epsabs=1e-13, epsrel=1e-13, limit=500)[0]
+        G = np.array([[q(lambda x, i=i, j=j: r[i](x) * r[j](x)) for j in range(3)] for i in range(3)])
+        b = np.array([q(lambda x, i=i: g(x) * r[i](x)) for i in range(3)])
+        K = np.block([[G, np.ones((3, 1))], [np.ones((1, 3)), np.zeros((1, 1))]])
+        w = np.linalg.solve(K, np.concatenate([b, [1.0]]))[:3]
+        assert np.allclose(t[2:], c, rtol=0, atol=0)
+        assert np.allclose(t[:2], w[:2], rtol=1e-7, atol=1e-9), (t[:2], w[:2])
+        assert float(J[0]) == pytest.approx(ofit.objective(act, 2, t, OBJ[obj]), rel=1e-9)
