@@ -247,3 +247,21 @@ def test_projection_weights_vs_kkt_solve(act, obj):
         assert np.allclose(t[2:], c, rtol=0, atol=0)
         assert np.allclose(t[:2], w[:2], rtol=1e-7, atol=1e-9), (t[:2], w[:2])
         assert float(J[0]) == pytest.approx(ofit.objective(act, 2, t, OBJ[obj]), rel=1e-9)
+
+
+def test_refine_in_place_matches_out_of_place():
+    """lmbp_fit_refine documents theta == theta_out as allowed."""
+    from paper_2406_16282_b200 import _lib
+    rng = np.random.default_rng(5)
+    th = torch.tensor(np.array([[0.1 * rng.standard_normal() - 0.05, 1.1 + 0.02 * rng.standard_normal(),
+                                 -3.0 + 0.2 * rng.standard_normal(), 0.01 * rng.standard_normal(),
+                                 3.0 + 0.2 * rng.standard_normal()] for _ in range(64)]),
+                      dtype=torch.float64, device=DEV)
+    best, out, J = ops.fit_refine(th.clone(), "gelu", iters=5)
+    inplace = th.clone()
+    J2 = torch.empty(64, dtype=torch.float64, device=DEV)
+    rc = _lib.lib().lmbp_fit_refine(0, 0, 2, 1e-8, inplace.data_ptr(), 64, 5, inplace.data_ptr(), J2.data_ptr(),
+                                    None, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert torch.equal(inplace, out) and torch.equal(J2, J)
