@@ -168,14 +168,16 @@ def test_projected_kbit_fits(act):
     assert Js[3] < plain.J
 
 
-def test_anneal_deterministic_and_launch_independent():
-    b1, t1, j1 = ops.fit_anneal("silu", chains=300, iters=200, seed=11)
-    b2, t2, j2 = ops.fit_anneal("silu", chains=300, iters=200, seed=11)
-    b3, t3, j3 = ops.fit_anneal("silu", chains=130, iters=200, seed=11)
+@pytest.mark.parametrize("projected", [False, True])
+def test_anneal_deterministic_and_launch_independent(projected):
+    kw = dict(projected=projected)
+    b1, t1, j1 = ops.fit_anneal("silu", chains=300, iters=200, seed=11, **kw)
+    b2, t2, j2 = ops.fit_anneal("silu", chains=300, iters=200, seed=11, **kw)
+    b3, t3, j3 = ops.fit_anneal("silu", chains=130, iters=200, seed=11, **kw)
     torch.cuda.synchronize()
     assert torch.equal(b1, b2) and torch.equal(t1, t2)
     assert torch.equal(t1[:130], t3) and torch.equal(j1[:130], j3)
-    b4, _, _ = ops.fit_anneal("silu", chains=300, iters=200, seed=12)
+    b4, _, _ = ops.fit_anneal("silu", chains=300, iters=200, seed=12, **kw)
     assert not torch.equal(b1, b4)
     assert float(b1[-1]) == float(j1.min())
 
