@@ -42,10 +42,29 @@ def _need(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
-def _stream(stream) -> int:
+def _stream(stream, dev: torch.device) -> int:
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(dev)
+    elif isinstance(stream, torch.cuda.Stream) and stream.device != dev:
+        raise ValueError(f"stream is on {stream.device}, tensors on {dev}")
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _device(fn: str, *ts: torch.Tensor) -> torch.device:
+    """The one device all tensors of a call live on (the library launches on
+    the current device, so a call is made with that device current)."""
+    dev = ts[0].device
+    for t in ts[1:]:
+        if t.device != dev:
+            raise ValueError(f"{fn}: tensors on different devices ({dev}, {t.device})")
+    return dev
+
+
+def _launch(fn: str, dev: torch.device, stream, *args) -> None:
+    """Call entry point fn(*args, stream) with dev current; raise on a status."""
+    s = _stream(stream, dev)
+    with torch.cuda.device(dev):
+        check(fn, getattr(lib(), fn)(*args, s))
 
 
 def _act_fwd(fn: str, x, y, codes, stream):
@@ -58,8 +77,8 @@ def _act_fwd(fn: str, x, y, codes, stream):
     rows, cols = _rc(x)
     if n == 0:
         return y, codes
-    check(fn, getattr(lib(), fn)(x.data_ptr(), y.data_ptr(), codes.data_ptr(), rows, cols, _dtype(x),
-                                 _stream(stream)))
+    _launch(fn, _device(fn, x, y, codes), stream, x.data_ptr(), y.data_ptr(), codes.data_ptr(), rows, cols,
+            _dtype(x))
     return y, codes
 
 
@@ -75,8 +94,8 @@ def _act_bwd(fn: str, dy, codes, dx, stream):
     rows, cols = _rc(dy)
     if n == 0:
         return dx
-    check(fn, getattr(lib(), fn)(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols, _dtype(dy),
-                                 _stream(stream)))
+    _launch(fn, _device(fn, dy, codes, dx), stream, dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols,
+            _dtype(dy))
     return dx
 
 
@@ -107,8 +126,8 @@ def _norm_fwd(fn, x, eps, y, rstd, stream):
     rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None else _need(rstd, "rstd")
     if y.shape != x.shape or y.dtype != x.dtype or rstd.numel() != rows or rstd.dtype != torch.float32:
         raise ValueError(f"{fn}: shape/dtype mismatch")
-    check(fn, getattr(lib(), fn)(x.data_ptr(), y.data_ptr(), rstd.data_ptr(), rows, cols, float(eps), _dtype(x),
-                                 _stream(stream)))
+    _launch(fn, _device(fn, x, y, rstd), stream, x.data_ptr(), y.data_ptr(), rstd.data_ptr(), rows, cols,
+            float(eps), _dtype(x))
     return y, rstd
 
 
@@ -121,8 +140,8 @@ def _norm_bwd(fn, dy, y, rstd, dx, stream):
     if y.shape != dy.shape or y.dtype != dy.dtype or rstd.numel() != rows or dx.shape != dy.shape \
             or rstd.dtype != torch.float32 or dx.dtype != dy.dtype:
         raise ValueError(f"{fn}: token/shape mismatch (S:L266)")
-    check(fn, getattr(lib(), fn)(dy.data_ptr(), y.data_ptr(), rstd.data_ptr(), dx.data_ptr(), rows, cols,
-                                 _dtype(dy), _stream(stream)))
+    _launch(fn, _device(fn, dy, y, rstd, dx), stream, dy.data_ptr(), y.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+            rows, cols, _dtype(dy))
     return dx
 
 
@@ -174,8 +193,8 @@ def reswiglu2_fwd(gate, up, h=None, a=None, codes=None, stream=None):
     rows, cols = _rc(gate)
     if n == 0:
         return h, a, codes
-    check("reswiglu2_fwd", lib().reswiglu2_fwd(gate.data_ptr(), up.data_ptr(), h.data_ptr(), a.data_ptr(),
-                                               codes.data_ptr(), rows, cols, _dtype(gate), _stream(stream)))
+    _launch("reswiglu2_fwd", _device("reswiglu2_fwd", gate, up, h, a, codes), stream, gate.data_ptr(),
+            up.data_ptr(), h.data_ptr(), a.data_ptr(), codes.data_ptr(), rows, cols, _dtype(gate))
     return h, a, codes
 
 
@@ -194,9 +213,8 @@ def reswiglu2_bwd(dh, up, a, codes, dgate=None, dup=None, stream=None):
     rows, cols = _rc(dh)
     if n == 0:
         return dgate, dup
-    check("reswiglu2_bwd", lib().reswiglu2_bwd(dh.data_ptr(), up.data_ptr(), a.data_ptr(), codes.data_ptr(),
-                                               dgate.data_ptr(), dup.data_ptr(), rows, cols, _dtype(dh),
-                                               _stream(stream)))
+    _launch("reswiglu2_bwd", _device("reswiglu2_bwd", dh, up, a, codes, dgate, dup), stream, dh.data_ptr(),
+            up.data_ptr(), a.data_ptr(), codes.data_ptr(), dgate.data_ptr(), dup.data_ptr(), rows, cols, _dtype(dh))
     return dgate, dup
 
 
@@ -226,9 +244,9 @@ def stepact_fwd(x, act: str, k: int, thresholds, y=None, codes=None, stream=None
     keep, ptr = _dbl(thresholds)
     if n == 0:
         return y, codes
-    check("stepact_fwd", lib().stepact_fwd({"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}[act], int(k), ptr,
-                                           x.data_ptr(), y.data_ptr(), codes.data_ptr(), rows, cols, _dtype(x),
-                                           _stream(stream)))
+    _launch("stepact_fwd", _device("stepact_fwd", x, y, codes), stream,
+            {"gelu": _lib.LMBP_GELU, "silu": _lib.LMBP_SILU}[act], int(k), ptr, x.data_ptr(), y.data_ptr(),
+            codes.data_ptr(), rows, cols, _dtype(x))
     return y, codes
 
 
@@ -244,8 +262,8 @@ def stepact_bwd(dy, codes, k: int, levels, dx=None, stream=None):
     keep, ptr = _dbl(levels)
     if n == 0:
         return dx
-    check("stepact_bwd", lib().stepact_bwd(int(k), ptr, dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), rows, cols,
-                                           _dtype(dy), _stream(stream)))
+    _launch("stepact_bwd", _device("stepact_bwd", dy, codes, dx), stream, int(k), ptr, dy.data_ptr(),
+            codes.data_ptr(), dx.data_ptr(), rows, cols, _dtype(dy))
     return dx
 
 
@@ -279,8 +297,8 @@ def fit_objective(theta, act: str, k: int = 2, objective: str = "h", eps: float 
     J = torch.empty(n, dtype=torch.float64, device=theta.device) if J is None else _need(J, "J")
     if J.dtype != torch.float64 or J.numel() != n:
         raise ValueError("J must be float64 [n]")
-    check("lmbp_fit_objective", lib().lmbp_fit_objective(_ACT[act], _OBJ[objective], int(k), float(eps),
-                                                         theta.data_ptr(), J.data_ptr(), n, _stream(stream)))
+    _launch("lmbp_fit_objective", _device("lmbp_fit_objective", theta, J), stream, _ACT[act], _OBJ[objective],
+            int(k), float(eps), theta.data_ptr(), J.data_ptr(), n)
     return J
 
 
@@ -300,10 +318,10 @@ def fit_anneal(act: str, k: int = 2, objective: str = "h", eps: float = 1e-8, ch
     chain_J = torch.empty(chains, dtype=torch.float64, device=device)
     best = torch.empty(P + 1, dtype=torch.float64, device=device)
     fn = "lmbp_fit_anneal_vp" if projected else "lmbp_fit_anneal"
-    check(fn, getattr(lib(), fn)(
-        _ACT[act], _OBJ[objective], int(k), float(eps), None if init is None else init.data_ptr(), int(chains),
-        int(iters), int(seed) & (2 ** 64 - 1), float(t0), float(t1), float(step0), float(step1),
-        chain_theta.data_ptr(), chain_J.data_ptr(), best.data_ptr(), _stream(stream)))
+    dev = _device(fn, chain_theta, *(() if init is None else (init,)))
+    _launch(fn, dev, stream, _ACT[act], _OBJ[objective], int(k), float(eps),
+            None if init is None else init.data_ptr(), int(chains), int(iters), int(seed) & (2 ** 64 - 1), float(t0),
+            float(t1), float(step0), float(step1), chain_theta.data_ptr(), chain_J.data_ptr(), best.data_ptr())
     return best, chain_theta, chain_J
 
 
@@ -318,7 +336,6 @@ def fit_refine(theta, act: str, k: int = 2, objective: str = "h", eps: float = 1
     out = torch.empty_like(theta)
     J = torch.empty(n, dtype=torch.float64, device=theta.device)
     best = torch.empty(P + 1, dtype=torch.float64, device=theta.device)
-    check("lmbp_fit_refine", lib().lmbp_fit_refine(_ACT[act], _OBJ[objective], int(k), float(eps), theta.data_ptr(),
-                                                   n, int(iters), out.data_ptr(), J.data_ptr(), best.data_ptr(),
-                                                   _stream(stream)))
+    _launch("lmbp_fit_refine", theta.device, stream, _ACT[act], _OBJ[objective], int(k), float(eps),
+            theta.data_ptr(), n, int(iters), out.data_ptr(), J.data_ptr(), best.data_ptr())
     return best, out, J
