@@ -100,6 +100,53 @@ def algorithmic_bytes(cfg, R):
             "norm_bwd": (3 * b * H + 4) * R}   # read dy, y, rstd; write dx
 
 
+def rw_bytes(cfg, R):
+    """(read, write) algorithmic bytes per kernel; sums to algorithmic_bytes."""
+    b = synth.ELEM_BYTES[cfg["dtype"]]
+    n = R * cfg["F"]
+    H = cfg["H"]
+    nc = (n + 3) // 4
+    return {"norm_fwd": (b * H * R, (b * H + 4) * R),
+            "act_fwd": (b * n, b * n + nc),
+            "act_bwd": (b * n + nc, b * n),
+            "norm_bwd": ((2 * b * H + 4) * R, b * H * R)}
+
+
+def rw_model_section(x, dy, dx, y, flush, sink, stream, kern, rw, iters=10):
+    """Direction-aware HBM model (DESIGN 5.3): time a torch copy (1 read : 1
+    write) and add (2 : 1) of the activation tensors with the bench protocol,
+    fit t = R/r + W/w, and rate every kernel against its own read/write mix.
+    Informational only: roofline.peak stays the driver's copy figure."""
+    def timeit(fn):
+        fn()
+        ts = []
+        for _ in range(iters):
+            sink.copy_(flush.sum())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        us = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
+        return us[len(us) // 2]
+
+    B = x.numel() * x.element_size()
+    t_copy = timeit(lambda: y.copy_(x))
+    t_add = timeit(lambda: torch.add(x, dy, out=dx))
+    tr = (t_add - t_copy) / B                  # us per byte read
+    tw = t_copy / B - tr                       # us per byte written
+    if not (tr > 0 and tw > 0):
+        return None
+    out = {"read_GBs": round(1e-3 / tr, 1), "write_GBs": round(1e-3 / tw, 1), "probe_bytes": B,
+           "copy_us": round(t_copy, 2), "add_us": round(t_add, 2), "kernels": {}}
+    for k, (rd, wr) in rw.items():
+        ideal = rd * tr + wr * tw
+        out["kernels"][k] = {"read": rd, "write": wr, "model_us": round(ideal, 2),
+                             "frac": round(ideal / kern[k]["us"], 4)}
+    return out
+
+
 def bytes_saved(cfg, R):
     b = synth.ELEM_BYTES[cfg["dtype"]]
     n = R * cfg["F"]
@@ -659,6 +706,9 @@ def main():
                "path": f"pinned host -> H2D -> C-ABI kernels -> D2H pinned host; {nchunk} row chunks "
                        f"round-robin on {len(streams)} streams (copies overlap kernels and each other)"}
 
+    rwb = rw_bytes(cfg, R)
+    assert all(sum(rwb[k]) == nbytes[k] for k in kernels)
+    rw_model = rw_model_section(x, dy, dx, y, flush, flush_sink, stream, kern, rwb)
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
     block = block_section(cfg, R, dev) if rank == 0 else None
     step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink, peak)
@@ -680,7 +730,7 @@ def main():
                        "arithmetic": f"binary32 in registers, {dt} storage (codes: 2-bit packed uint8)",
                        "l2": "flushed before every kernel by reading a 2x L2 buffer (L2 left clean), outside the CUDA events",
                        "parallelism": f"dp{world} (rows per rank, no data-path collective)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "rw_model": rw_model, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),
             "fraction_of_8TBs": round(value / world / NOMINAL_HBM_GBS, 4),
