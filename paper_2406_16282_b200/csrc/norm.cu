@@ -367,6 +367,9 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+#ifndef LMBP_ROW_UNIT
+#define LMBP_ROW_UNIT 1
+#endif
 template <typename T, int NORM, bool kFwd, int V>
 __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 *b, const float *rstd_in, uint4 *out,
                                                     float *rstd_out, int64_t rows, int nvec, int cols, float eps,
@@ -398,33 +401,39 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
 
   if (warp == W) {  // producer
     if (lane == 0) {
-      int64_t row = blockIdx.x;
       // backward: the producer loads the row's rstd (issued a row ahead, so
       // the load's latency hides behind the stage wait) and hands it over in
       // the stage's slot; the consumers never wait on global memory.
+      // Work unit u = rows [u R, min(rows, (u + 1) R)), R = LMBP_ROW_UNIT.
+      int64_t row = (int64_t)blockIdx.x * LMBP_ROW_UNIT;
       float rnext = 0.0f;
       if constexpr (!kFwd) rnext = rstd_in[row];
       uint32_t ph = 0;
       int k = 0;
-      for (;; ++k) {
+      for (;;) {
         mbar_arrive_expect_tx(clc_bar, 16);
         clc_try_cancel(clc_resp, clc_bar);
-        const int s = k % stages;
-        mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
-        slot[s] = row;
-        if constexpr (!kFwd) rslot[s] = rnext;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-        uint8_t *st = smem + (size_t)s * stage_bytes;
-        bulk_g2s(st, a + row * nvec, (uint32_t)row_bytes, &full[s]);
-        if constexpr (!kFwd) bulk_g2s(st + row_bytes, b + row * nvec, (uint32_t)row_bytes, &full[s]);
+        const int64_t row_end = min(rows, row + LMBP_ROW_UNIT);
+        for (; row < row_end; ++row, ++k) {
+          const int s = k % stages;
+          mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
+          slot[s] = row;
+          if constexpr (!kFwd) {
+            rslot[s] = rnext;
+            if (row + 1 < row_end) rnext = rstd_in[row + 1];
+          }
+          mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+          uint8_t *st = smem + (size_t)s * stage_bytes;
+          bulk_g2s(st, a + row * nvec, (uint32_t)row_bytes, &full[s]);
+          if constexpr (!kFwd) bulk_g2s(st + row_bytes, b + row * nvec, (uint32_t)row_bytes, &full[s]);
+        }
         mbar_wait(clc_bar, ph);
         ph ^= 1u;
         const int next = clc_query(clc_resp);
         if (next < 0) break;
-        row = next;
+        row = (int64_t)next * LMBP_ROW_UNIT;
         if constexpr (!kFwd) rnext = rstd_in[row];
       }
-      ++k;
       const int s = k % stages;
       mbar_wait(&empty[s], ((uint32_t)(k / stages) & 1u) ^ 1u);
       slot[s] = -1;
@@ -563,12 +572,18 @@ struct RowTmaPlan {
 static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   RowTmaPlan p{false, 0, 0, 0, 0};
   if (nvec < 256 || nvec > 16 * 32 * 8) return p;
-  int warps = (int)((nvec + 4 * 32 - 1) / (4 * 32));  // aim for 4 vectors per thread
+#ifndef LMBP_ROW_VAIM
+#define LMBP_ROW_VAIM 4
+#endif
+#ifndef LMBP_ROW_STAGE_KB
+#define LMBP_ROW_STAGE_KB 96
+#endif
+  int warps = (int)((nvec + LMBP_ROW_VAIM * 32 - 1) / (LMBP_ROW_VAIM * 32));  // aim for 4 vectors per thread
   if (warps > 16) warps = 16;
   const int V = (int)((nvec + warps * 32 - 1) / (warps * 32));
   if (V > 8) return p;
   const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
-  int stages = (int)std::min<size_t>(4, (size_t)(96 * 1024) / stage);
+  int stages = (int)std::min<size_t>(4, (size_t)(LMBP_ROW_STAGE_KB * 1024) / stage);
   if (stages < 2) stages = 2;
   const size_t tail = 16 + (2 * (size_t)stages + 1) * 8 + (size_t)stages * 8 + 64 * sizeof(float2) +
                       (size_t)stages * sizeof(float);
@@ -589,8 +604,9 @@ static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const v
   static std::atomic<unsigned long long> smem_set{0};
   const cudaError_t e = ensure_dyn_smem(kern, 227 * 1024, smem_set);
   if (e != cudaSuccess) return e;
-  if (rows > 0x7fffffff) return cudaErrorInvalidValue;
-  kern<<<(int)rows, (rp.warps + 1) * 32, rp.smem, s>>>(reinterpret_cast<const uint4 *>(a),
+  const int64_t units = (rows + LMBP_ROW_UNIT - 1) / LMBP_ROW_UNIT;
+  if (units > 0x7fffffff) return cudaErrorInvalidValue;
+  kern<<<(int)units, (rp.warps + 1) * 32, rp.smem, s>>>(reinterpret_cast<const uint4 *>(a),
                                                         reinterpret_cast<const uint4 *>(b), rstd_in,
                                                         reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec,
                                                         (int)cols, eps, rp.stages);
