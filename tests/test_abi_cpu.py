@@ -125,6 +125,15 @@ def test_binding_refuses_cpu_tensors():
         ops.msrms_fwd(torch.zeros(2, 4))
 
 
+def test_binding_refuses_mixed_devices():
+    """Every call runs on one device (the C ABI launches on the current one)."""
+    import torch
+    a, b = torch.zeros(4), torch.zeros(4, device="meta")
+    assert ops._device("f", a, a) == a.device
+    with pytest.raises(ValueError, match="different devices"):
+        ops._device("f", a, b)
+
+
 def test_product_package_does_not_import_oracle():
     """The product path never touches oracle/ (no CPU fallback)."""
     pkg = os.path.join(ROOT, "paper_2406_16282_b200")
