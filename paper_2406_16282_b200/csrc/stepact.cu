@@ -17,8 +17,24 @@
 #include "ew_pipeline.cuh"
 #include "kernels.h"
 
+// Forward pipeline shape (tools/sweep.py): consumer warps x vectors x stages,
+// and for k = 4 the CTAs per SM the register budget must allow.
+#ifndef LMBP_STEP_W
+#define LMBP_STEP_W 16
+#define LMBP_STEP_U 2
+#define LMBP_STEP_S 4
+#endif
+#ifndef LMBP_STEP4_W  // k = 4, 16-bit types
+#define LMBP_STEP4_W 12
+#endif
+#ifndef LMBP_STEP4_S
+#define LMBP_STEP4_S 3
+#endif
 #ifndef LMBP_STEP_MINB4
-#define LMBP_STEP_MINB4 2
+#define LMBP_STEP_MINB4 3
+#endif
+#ifndef LMBP_STEP_MINB4_F32
+#define LMBP_STEP_MINB4_F32 2
 #endif
 
 namespace lmbp {
@@ -207,11 +223,17 @@ __device__ __forceinline__ uint32_t step_codes_vec(const uint4 &r, const float *
 template <typename T, int A, bool kPrecise, int K>
 struct StepFwdOp {
   using Params = StepEwParams;
-  // 2 CTAs / SM (<= 60 registers): at k = 4 the 15 hoisted packed thresholds
-  // would otherwise take the kernel to 72 registers and 1 CTA / SM.
-  static constexpr int kMinBlocks = K == 4 ? LMBP_STEP_MINB4 : 0;
+  // k = 4 register budget: the 15 hoisted thresholds would otherwise take the
+  // kernel to 72+ registers and fewer warps per SM.  16-bit types: 12
+  // consumer warps x 3 stages, 3 CTAs / SM (<= 48 registers) for SiLU; GELU
+  // (it would spill at 48) and fp32: 16 x 4, 2 CTAs / SM (profiles/r01/sweep32_*, sweep33_*: C4 96.4 -> 94.3 us,
+  // C5 443 -> 429 us; the 16-bit shape costs C3 fp32 +2 %, so fp32 keeps its own).
+  static constexpr bool k16 = sizeof(T) == 2 && A == kActSilu;  // GELU's math needs > 48 registers
+  static constexpr int kMinBlocks = K == 4 ? (k16 ? LMBP_STEP_MINB4 : LMBP_STEP_MINB4_F32) : 0;
   static constexpr int kVecT = Traits<T>::kVec;
-  static constexpr int W = 16, U = 2, S = 4, kIn = 1, kCodeIn = 0, kCodeOut = kVecT * K / 8;
+  static constexpr int W = K == 4 && k16 ? LMBP_STEP4_W : LMBP_STEP_W, U = LMBP_STEP_U,
+                       S = K == 4 && k16 ? LMBP_STEP4_S : LMBP_STEP_S, kIn = 1, kCodeIn = 0,
+                       kCodeOut = kVecT * K / 8;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p) {
     float f[kVecT];
     Vec<T>::unpack(v[0], f);

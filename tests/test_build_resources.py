@@ -44,3 +44,19 @@ def test_no_spills_in_hot_kernels():
         text = open(os.path.join(OBJ, log)).read()
         spills = [int(x) for x in re.findall(r"(\d+) bytes spill stores", text)]
         assert max(spills) == 0, log
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "stepact.ptxas.log")), reason="no build logs")
+def test_kbit_forward_register_budget():
+    """k = 4 SiLU forward, 16-bit types: 13-warp CTAs (416 threads), 3 per SM
+    need <= 52 registers (ptxas targets 48); no step forward spills (sweep33)."""
+    r = regs("stepact.ptxas.log")
+    d = demangle(list(r))
+    by = {d[k]: v for k, v in r.items()}
+    k4 = [v for k, v in by.items() if re.search(r"StepFwdOp<(__nv_bfloat16|__half), 1, false, 4>", k)]
+    assert len(k4) == 2, by
+    assert max(k4) <= 52, by
+    text = open(os.path.join(OBJ, "stepact.ptxas.log")).read()
+    for m in re.finditer(r"Function properties for (\S+)\n.*?(\d+) bytes spill stores", text):
+        if "StepFwdOp" in demangle([m.group(1)])[m.group(1)]:
+            assert int(m.group(2)) == 0, m.group(1)
