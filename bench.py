@@ -626,14 +626,19 @@ def main():
                    "frac_of_8TBs": round(gbs / NOMINAL_HBM_GBS, 4),
                    "share": round(sum(per_kernel[k]) / total_ms, 4)}
     dom = max(kernels, key=lambda k: kern[k]["us"])
-    traffic = None
+    traffic = l2w = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath)).get(args.config, {})
-        traffic = tr.get(dom)
+        tj = json.load(open(tpath))
+        traffic = tj.get(args.config, {}).get(dom)
+        l2w = tj.get(args.config + "_detail", {}).get(dom, {}).get("l2_write_from_sm")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GB/s"], "peak": peak, "unit": "GB/s",
                 "frac": kern[dom]["frac"], "traffic": traffic, "algorithmic_bytes": nbytes[dom],
-                "peak_source": peak_src, "frac_of_8TBs": kern[dom]["frac_of_8TBs"]}
+                "peak_source": peak_src, "frac_of_8TBs": kern[dom]["frac_of_8TBs"],
+                "traffic_note": "ncu dram read+write per launch; DRAM writes still dirty in L2 at kernel end are "
+                                "not counted, so l2_write_bytes (every byte the SMs stored, from the same capture) "
+                                "is the write side to compare with the algorithmic bytes",
+                "l2_write_bytes": l2w}
 
     # e2e through the public API with host buffers: H2D inputs, 4 kernels, D2H results
     e2e = None

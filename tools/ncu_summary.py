@@ -16,6 +16,7 @@ KEYS = {
     "duration_us": "gpu__time_duration.sum",
     "dram_read_B": "dram__bytes_read.sum",
     "dram_write_B": "dram__bytes_write.sum",
+    "l2_write_sectors": "lts__t_sectors_srcunit_tex_op_write.sum",
     "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -92,11 +93,13 @@ def main():
         order = ["norm_fwd", "act_fwd", "act_bwd", "norm_bwd"]
         for slot, k in zip(order, kernels[:4]):
             entry[slot] = {"kernel": k["kernel"], "dram_bytes": k.get("dram_read_B", 0) + k.get("dram_write_B", 0),
-                           "dram_read": k.get("dram_read_B", 0), "dram_write": k.get("dram_write_B", 0)}
+                           "dram_read": k.get("dram_read_B", 0), "dram_write": k.get("dram_write_B", 0),
+                           "l2_write_from_sm": 32.0 * k.get("l2_write_sectors", 0)}
         tr[cfg] = {s: v["dram_bytes"] for s, v in entry.items()}
         tr[cfg + "_detail"] = entry
         tr["_note"] = ("ncu --set full, cache control all (cold L2), one launch per kernel in bench step order; "
-                       "DRAM writes still resident in L2 at kernel end are not counted by ncu")
+                       "DRAM writes still resident in L2 at kernel end are not counted by ncu; l2_write_from_sm "
+                       "(lts__t_sectors_srcunit_tex_op_write x 32 B) is every byte the kernel stored")
         json.dump(tr, open(path, "w"), indent=1)
 
 
