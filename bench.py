@@ -60,7 +60,53 @@ def parse(argv=None):
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the full config (its own batch); "
                          "strong: the config's rows are split across ranks")
+    ap.add_argument("--strong-config", default="c5", choices=sorted(synth.CONFIGS),
+                    help="config of the row-sharded strong-scaling key (north_star: C5)")
+    ap.add_argument("--strong-steps", type=int, default=10)
+    ap.add_argument("--no-strong", action="store_true", help="skip the strong-scaling (row-sharded C5) key")
     return ap.parse_args(argv)
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_cmd(gpus: int, argv, port: int, script: str = None):
+    """The torchrun command that re-runs this script as `gpus` ranks (one
+    process per GPU) on this node, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(gpus),
+            "--master-addr", "127.0.0.1", "--master-port", str(port),
+            script or os.path.abspath(__file__)] + list(argv)
+
+
+def self_launch(args, argv) -> int:
+    """`bench.py --gpus N` called directly (no WORLD_SIZE in the environment)
+    with N > 1: re-exec under torch.distributed.run so N ranks really run.
+    NCCL's init log (rank / nranks per communicator) stays on, on stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    import subprocess
+    return subprocess.call(launch_cmd(args.gpus, argv, _free_port()), env=env)
+
+
+def strong_summary(bytes_per_rank, ms_per_rank, steps, t1_ms=None):
+    """Row-sharded (strong) scaling numbers: aggregate GB/s = bytes of all
+    ranks / slowest rank, and t1 / (N tN) when the 1-GPU time is known."""
+    N = len(ms_per_rank)
+    tN = max(ms_per_rank) / steps
+    out = {"n_ranks": N, "per_rank_ms_per_step": [round(m / steps, 4) for m in ms_per_rank],
+           "ms_per_step": round(tN, 4), "GB/s": round(aggregate(bytes_per_rank, ms_per_rank, steps), 1),
+           "rank_spread": round(max(ms_per_rank) / min(ms_per_rank) - 1, 4) if min(ms_per_rank) > 0 else None}
+    if t1_ms is not None:
+        out["t1_ms_per_step"] = round(t1_ms, 4)
+        out["t1_over_N_tN"] = round(t1_ms / (N * tN), 4)
+    return out
 
 
 def shard_rows(R: int, world: int, rank: int, scaling: str):
@@ -276,6 +322,18 @@ def measured_hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def cpu_sockets():
+    """Physical packages (sockets) of the host, from sysfs."""
+    import glob
+    ids = set()
+    for p in glob.glob("/sys/devices/system/cpu/cpu[0-9]*/topology/physical_package_id"):
+        try:
+            ids.add(open(p).read().strip())
+        except OSError:
+            pass
+    return len(ids) or None
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -299,6 +357,7 @@ def cpu_baseline(cfg, eps, target_s):
             "sample": f"{rows} of {cfg['R']} rows of {cfg['desc']}: norm fwd+bwd and act fwd+bwd, float64 "
                       f"oracle incl. storage decode/encode, {sec:.2f} s",
             "seconds": round(sec, 3), "rows": rows, "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "sockets": cpu_sockets(),
             "single_core": {"value": round(nbytes1 / sec1 / 1e9, 4), "unit": "GB/s", "rows": rows1,
                             "seconds": round(sec1, 3)}}
 
@@ -524,17 +583,134 @@ def block_section(cfg, R, dev):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def main():
-    args = parse()
+KERNELS = ["norm_fwd", "act_fwd", "act_bwd", "norm_bwd"]
+
+
+class Workload:
+    """One rank's rows [row0, row0 + R) of a config, resident in HBM, and the
+    four launches of one step (norm fwd -> act fwd -> act bwd ->
+    norm bwd) through the C-ABI binding."""
+
+    def __init__(self, P, cfg, row0, R, dev, stream, eps):
+        F, H, dt = cfg["F"], cfg["H"], cfg["dtype"]
+        self.cfg, self.R, self.dev, self.stream, self.eps = cfg, R, dev, stream, eps
+        self.act_fwd, self.act_bwd = ((P.regelu2_fwd, P.regelu2_bwd) if cfg["act"] == "gelu"
+                                      else (P.resilu2_fwd, P.resilu2_bwd))
+        self.norm_fwd, self.norm_bwd = ((P.msln_fwd, P.msln_bwd) if cfg["norm"] == "ln"
+                                        else (P.msrms_fwd, P.msrms_bwd))
+        self.x = synth.act_input(R, F, dt, row_start=row0, device=dev)
+        self.dy = synth.grad_input(R, F, dt, row_start=row0, device=dev)
+        self.xn = synth.norm_input(R, H, dt, row_start=row0, device=dev)
+        self.gn = synth.grad_input(R, H, dt, row_start=row0, device=dev, stream=synth.S_NORM_DY)
+        self.y, self.dx = torch.empty_like(self.x), torch.empty_like(self.dy)
+        self.codes = torch.empty(P.codes_bytes(R * F), dtype=torch.uint8, device=dev)
+        self.yn, self.dxn = torch.empty_like(self.xn), torch.empty_like(self.gn)
+        self.rstd = torch.empty(R, dtype=torch.float32, device=dev)
+        s = stream
+        self.launch = {
+            "norm_fwd": lambda: self.norm_fwd(self.xn, eps, y=self.yn, rstd=self.rstd, stream=s),
+            "act_fwd": lambda: self.act_fwd(self.x, y=self.y, codes=self.codes, stream=s),
+            "act_bwd": lambda: self.act_bwd(self.dy, self.codes, dx=self.dx, stream=s),
+            "norm_bwd": lambda: self.norm_bwd(self.gn, self.yn, self.rstd, dx=self.dxn, stream=s),
+        }
+        self.nbytes = algorithmic_bytes(cfg, R)
+
+    def step(self, flush, sink, evs=None):
+        for i, k in enumerate(KERNELS):
+            sink.copy_(flush.sum())                    # evict L2 by reading 2 x L2 (outside the events)
+            if evs is not None:
+                evs[2 * i].record(self.stream)
+            self.launch[k]()
+            if evs is not None:
+                evs[2 * i + 1].record(self.stream)
+
+    def timed(self, flush, sink, steps, warmup, world, sampler=None):
+        """W untimed steps, then `steps` steps bracketed by barrier +
+        synchronize; returns {kernel: [ms per launch]}."""
+        for _ in range(max(3, warmup)):
+            self.step(flush, sink)
+        torch.cuda.synchronize()
+        events = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(steps)]
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        if sampler is not None:
+            sampler.start()
+        for s in range(steps):
+            self.step(flush, sink, events[s])
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        return {k: [events[s][2 * i].elapsed_time(events[s][2 * i + 1]) for s in range(steps)]
+                for i, k in enumerate(KERNELS)}
+
+    def free(self):
+        for k in ("x", "dy", "xn", "gn", "y", "dx", "codes", "yn", "dxn", "rstd"):
+            setattr(self, k, None)
+
+
+def gather_floats(vals, world, cdev):
+    t = torch.tensor(vals, dtype=torch.float64, device=cdev)
+    if world == 1:
+        return [t.tolist()]
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    torch.distributed.all_gather(parts, t)
+    return [p.tolist() for p in parts]
+
+
+def strong_section(P, args, world, rank, dev, stream, flush, sink, cdev):
+    """north_star / SURVEY 8(e): the strong-scaling configuration (C5,
+    LLaMA-13B shapes) with its R rows split into contiguous blocks, rank r
+    owning rows [r R / N, (r + 1) R / N).  Each rank times its shard (barrier-
+    aligned); with N > 1, rank 0 then also runs all R rows alone on its GPU so
+    t1 / (N tN) comes from the same box and run."""
+    cfg = synth.CONFIGS[args.strong_config]
+    row0, R = shard_rows(cfg["R"], world, rank, "strong")
+    w = Workload(P, cfg, row0, R, dev, stream, args.eps)
+    pk = w.timed(flush, sink, args.strong_steps, 3, world)
+    ms = sum(sum(v) for v in pk.values())
+    nb = sum(w.nbytes.values())
+    parts = gather_floats([ms, float(nb), float(row0), float(R)], world, cdev)
+    w.free()
+    torch.cuda.empty_cache()
+    t1 = None
+    if world == 1:
+        t1 = ms / args.strong_steps
+    else:
+        if rank == 0:
+            w1 = Workload(P, cfg, 0, cfg["R"], dev, stream, args.eps)
+            pk1 = w1.timed(flush, sink, args.strong_steps, 3, 1)
+            t1 = sum(sum(v) for v in pk1.values()) / args.strong_steps
+            w1.free()
+            torch.cuda.empty_cache()
+        torch.distributed.barrier()
+    if rank != 0:
+        return None
+    out = strong_summary([p[1] for p in parts], [p[0] for p in parts], args.strong_steps, t1)
+    out.update({"config": f"{args.strong_config}: {cfg['desc']}", "rows_total": cfg["R"],
+                "shards": [[int(p[2]), int(p[3])] for p in parts], "steps": args.strong_steps,
+                "partition": "contiguous row blocks, rank r owns rows [r*R/N, (r+1)*R/N); no data-path collective",
+                "t1": "rank 0 alone on all rows, same run" if world > 1 else "this run"})
+    return out
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else list(argv)
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args, argv)
     if args.impl == "reference":
         return run_reference(args)
     world, rank, local = dist_env()
-    # one process per GPU; --dist-backend gloo (with ranks sharing a device via
-    # local % device_count) exists only to exercise the N > 1 path on one GPU.
-    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    ndev = max(1, torch.cuda.device_count())
+    # one process per GPU.  NCCL cannot put two ranks on one device, so when
+    # there are more ranks than GPUs (exercising N > 1 on a one-GPU box) the
+    # ranks share devices (local % ndev) and the timing collectives use gloo.
+    dev = torch.device("cuda", local % ndev)
     torch.cuda.set_device(dev)
+    backend = args.dist_backend if world <= ndev else "gloo"
     if world > 1:
-        if args.dist_backend == "nccl":
+        if backend == "nccl":
             torch.distributed.init_process_group("nccl", device_id=dev)
         else:
             torch.distributed.init_process_group("gloo")
@@ -544,17 +720,6 @@ def main():
     cfg = synth.CONFIGS[args.config]
     F, H, dt = cfg["F"], cfg["H"], cfg["dtype"]
     row0, R = shard_rows(cfg["R"], world, rank, args.scaling)
-    act_fwd, act_bwd = (P.regelu2_fwd, P.regelu2_bwd) if cfg["act"] == "gelu" else (P.resilu2_fwd, P.resilu2_bwd)
-    norm_fwd, norm_bwd = (P.msln_fwd, P.msln_bwd) if cfg["norm"] == "ln" else (P.msrms_fwd, P.msrms_bwd)
-
-    x = synth.act_input(R, F, dt, row_start=row0, device=dev)
-    dy = synth.grad_input(R, F, dt, row_start=row0, device=dev)
-    xn = synth.norm_input(R, H, dt, row_start=row0, device=dev)
-    gn = synth.grad_input(R, H, dt, row_start=row0, device=dev, stream=synth.S_NORM_DY)
-    y, dx = torch.empty_like(x), torch.empty_like(dy)
-    codes = torch.empty(P.codes_bytes(R * F), dtype=torch.uint8, device=dev)
-    yn, dxn = torch.empty_like(xn), torch.empty_like(gn)
-    rstd = torch.empty(R, dtype=torch.float32, device=dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     # L2 flush: READ a buffer of 2 x L2.  A read leaves L2 holding clean lines
     # only, so the timed kernel neither hits its inputs in L2 nor pays for
@@ -562,55 +727,24 @@ def main():
     flush = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    cdev = dev if backend == "nccl" else torch.device("cpu")
 
-    kernels = ["norm_fwd", "act_fwd", "act_bwd", "norm_bwd"]
-    launch = {
-        "norm_fwd": lambda: norm_fwd(xn, args.eps, y=yn, rstd=rstd, stream=stream),
-        "act_fwd": lambda: act_fwd(x, y=y, codes=codes, stream=stream),
-        "act_bwd": lambda: act_bwd(dy, codes, dx=dx, stream=stream),
-        "norm_bwd": lambda: norm_bwd(gn, yn, rstd, dx=dxn, stream=stream),
-    }
+    w = Workload(P, cfg, row0, R, dev, stream, args.eps)
+    x, dy, xn, gn, y, dx = w.x, w.dy, w.xn, w.gn, w.y, w.dx
+    codes, yn, dxn, rstd = w.codes, w.yn, w.dxn, w.rstd
+    norm_fwd, norm_bwd, act_fwd, act_bwd = w.norm_fwd, w.norm_bwd, w.act_fwd, w.act_bwd
+    kernels = KERNELS
 
-    def step(evs=None):
-        for i, k in enumerate(kernels):
-            flush_sink.copy_(flush.sum())               # evict L2 by reading 2 x L2 (outside the events)
-            if evs is not None:
-                evs[2 * i].record(stream)
-            launch[k]()
-            if evs is not None:
-                evs[2 * i + 1].record(stream)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    events = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
     sampler = ClockSampler(dev.index if os.environ.get("CUDA_VISIBLE_DEVICES") is None else local)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    for s in range(args.steps):
-        step(events[s])
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    per_kernel = w.timed(flush, flush_sink, args.steps, args.warmup, world, sampler)
     clocks = sampler.stop()
 
-    per_kernel = {k: [events[s][2 * i].elapsed_time(events[s][2 * i + 1]) for s in range(args.steps)]
-                  for i, k in enumerate(kernels)}
     total_ms = sum(sum(v) for v in per_kernel.values())
-    nbytes = algorithmic_bytes(cfg, R)
+    nbytes = w.nbytes
     step_bytes = sum(nbytes.values())
-    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
-    t = torch.tensor([total_ms, float(step_bytes)], dtype=torch.float64, device=cdev)
-    if world > 1:
-        parts = [torch.zeros_like(t) for _ in range(world)]
-        torch.distributed.all_gather(parts, t)
-    else:
-        parts = [t]
-    ms_all = [float(p[0]) for p in parts]
-    bytes_all = [float(p[1]) for p in parts]
+    parts = gather_floats([total_ms, float(step_bytes)], world, cdev)
+    ms_all = [p[0] for p in parts]
+    bytes_all = [p[1] for p in parts]
     max_ms = max(ms_all)
     value = aggregate(bytes_all, ms_all, args.steps)
 
@@ -620,9 +754,11 @@ def main():
     for k in kernels:
         avg = sum(per_kernel[k]) / len(per_kernel[k])
         gbs = nbytes[k] / (avg / 1e3) / 1e9
-        kern[k] = {"us": round(avg * 1e3, 2), "us_p10": round(1e3 * float(np.percentile(per_kernel[k], 10)), 2),
+        kern[k] = {"us": round(avg * 1e3, 2), "us_median": round(1e3 * float(np.median(per_kernel[k])), 2),
+                   "us_p10": round(1e3 * float(np.percentile(per_kernel[k], 10)), 2),
                    "us_p90": round(1e3 * float(np.percentile(per_kernel[k], 90)), 2),
                    "bytes": nbytes[k], "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
+                   "GB/s_median": round(nbytes[k] / (float(np.median(per_kernel[k])) / 1e3) / 1e9, 1),
                    "frac_of_8TBs": round(gbs / NOMINAL_HBM_GBS, 4),
                    "share": round(sum(per_kernel[k]) / total_ms, 4)}
     dom = max(kernels, key=lambda k: kern[k]["us"])
@@ -720,6 +856,8 @@ def main():
     fitter = fitter_section(stream, cpu=(world == 1 and not args.no_cpu_baseline)) if (
         rank == 0 and not args.no_fitter) else None
 
+    strong = None if args.no_strong else strong_section(P, args, world, rank, dev, stream, flush, flush_sink, cdev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.eps, args.cpu_seconds)
@@ -734,7 +872,9 @@ def main():
                        "step": "norm_fwd, act_fwd, act_bwd, norm_bwd",
                        "arithmetic": f"binary32 in registers, {dt} storage (codes: 2-bit packed uint8)",
                        "l2": "flushed before every kernel by reading a 2x L2 buffer (L2 left clean), outside the CUDA events",
-                       "parallelism": f"dp{world} (rows per rank, no data-path collective)"},
+                       "parallelism": f"dp{world} (rows per rank, no data-path collective)",
+                       "dist_backend": backend if world > 1 else None,
+                       "devices": min(world, ndev)},
             "roofline": roofline, "rw_model": rw_model, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),
@@ -742,6 +882,7 @@ def main():
             "elements_per_s": round(sum(bytes_all) / step_bytes * (R * F * 2 + R * H * 2) * args.steps
                                     / (max_ms / 1e3), 1),
             "per_rank_ms": [round(m, 3) for m in ms_all],
+            "strong_c5": strong,
             "activation_bytes_saved_per_layer": bytes_saved(cfg, R),
             "reswiglu2": swiglu,
             "activation_bytes_saved_per_block": block,

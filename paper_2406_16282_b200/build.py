@@ -35,13 +35,23 @@ def _stale(target: str, deps) -> bool:
 def _compile(src: str, objdir: str = OBJ, defines=()) -> str:
     obj = os.path.join(objdir, src.replace(".cu", ".o"))
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
-    if _stale(obj, deps):
+    stamp = obj.replace(".o", ".defines")
+    want = "\n".join(sorted(defines))
+    try:
+        have = open(stamp).read()
+    except OSError:
+        have = None
+    if _stale(obj, deps) or have != want:     # a changed -D set is stale too
+        if os.path.exists(stamp):
+            os.remove(stamp)
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(obj.replace(".o", ".ptxas.log"), "w") as f:
             f.write(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
+        with open(stamp, "w") as f:
+            f.write(want)
     return obj
 
 
@@ -63,12 +73,15 @@ def build(force: bool = False) -> str:
 def build_variant(name: str, defines) -> str:
     """Tuning aid: build liblmbp_<name>.so with extra -D defines into
     _variants/ (used by tools/sweep.py; the product library is LIB)."""
+    import hashlib
+    tag = hashlib.sha1("\n".join(sorted(defines)).encode()).hexdigest()[:8]
+    name = f"{name}-{tag}"                     # same name, different -D set: a different build
     vdir = os.path.join(HERE, "_variants", name)
     os.makedirs(vdir, exist_ok=True)
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, vdir, defines), SOURCES))
     out = os.path.join(HERE, "_variants", f"liblmbp_{name}.so")
-    if _stale(out, objs):
+    if _stale(out, objs) or not os.path.exists(out):
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
     return out
 

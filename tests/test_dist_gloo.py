@@ -83,3 +83,43 @@ def test_sharded_codes_equal_single_process(R):
     assert np.array_equal(got, full)
     assert ms == [10.0, 11.0] and sum(nbytes) == R * F
     assert bench.aggregate(nbytes, ms, 1) == pytest.approx(R * F / 0.011 / 1e9)
+
+
+def test_self_launch_command_runs_n_ranks(tmp_path):
+    """bench.py --gpus N without WORLD_SIZE re-execs itself under
+    torch.distributed.run (bench.launch_cmd); the command must bring up N
+    ranks that rendezvous on 127.0.0.1 and see WORLD_SIZE = N."""
+    import json
+    import subprocess
+    import sys
+    script = tmp_path / "probe.py"
+    script.write_text(
+        "import json, os, torch.distributed as dist\n"
+        "dist.init_process_group('gloo')\n"
+        "r, w = dist.get_rank(), dist.get_world_size()\n"
+        "out = [None] * w\n"
+        "dist.all_gather_object(out, (r, int(os.environ['LOCAL_RANK'])))\n"
+        "if r == 0:\n"
+        "    print(json.dumps({'world': w, 'ranks': out, 'argv': __import__('sys').argv[1:]}))\n"
+        "dist.destroy_process_group()\n")
+    argv = ["--gpus", "2", "--steps", "3"]
+    cmd = bench.launch_cmd(2, argv, _free_port(), script=str(script))
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["world"] == 2 and sorted(line["ranks"]) == [[0, 0], [1, 1]] and line["argv"] == argv
+
+
+def test_strong_summary():
+    s = bench.strong_summary([2e9, 2e9], [10.0, 12.5], 10, t1_ms=2.0)
+    assert s["n_ranks"] == 2 and s["ms_per_step"] == 1.25
+    assert s["GB/s"] == pytest.approx(4e9 * 10 / 0.0125 / 1e9, rel=1e-4)
+    assert s["t1_over_N_tN"] == pytest.approx(2.0 / (2 * 1.25), abs=1e-4)
+    assert s["rank_spread"] == pytest.approx(0.25)
+    # C5's 32768 rows split evenly for N = 1, 2, 4, 8 and F % 4 == 0, so shard codes concatenate
+    c5 = synth.CONFIGS["c5"]
+    for n in (1, 2, 4, 8):
+        assert all(bench.shard_rows(c5["R"], n, r, "strong")[1] == c5["R"] // n for r in range(n))
+    assert c5["F"] % 4 == 0

@@ -286,13 +286,18 @@ def sample_rows(R, k=48, seed=0):
     return sorted(set([0, 1, R - 1] + list(rng.choice(R, size=min(k, R), replace=False))))
 
 
+@pytest.mark.parametrize("mode", ["bench", "coverage"])
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
-def test_full_size_sampled(cfg):
+def test_full_size_sampled(cfg, mode):
+    """Full BASELINE sizes in bench.py's launch configuration; rows sampled
+    over the whole tensor, so tiles taken over by cluster-launch-control work
+    stealing are among them.  Coverage-mode inputs (10 % U(-12, 12)) put all
+    four segments -- SiLU's outer ones sit at +-6.3 -- on those tiles."""
     c = synth.CONFIGS[cfg]
     R, F, H, dtype = c["R"], c["F"], c["H"], c["dtype"]
     fwd, bwd = ACT[c["act"]]
     nf, nb, of, ob = NORM[c["norm"]]
-    x = synth.act_input(R, F, dtype, device=DEV)
+    x = synth.act_input(R, F, dtype, device=DEV, mode=mode)
     dy = synth.grad_input(R, F, dtype, device=DEV)
     y, codes = fwd(x)
     dx = bwd(dy, codes)
@@ -312,6 +317,9 @@ def test_full_size_sampled(cfg):
     x_s, dy_s = x[idx].cpu(), dy[idx].cpu()
     c_ref = check_act_fwd(c["act"], dtype, x_s, y[idx], cb.reshape(-1))
     check_act_bwd(c["act"], dtype, c_ref, dy_s, dx[idx])
+    if mode == "coverage":
+        seg = np.bincount(((c_ref[:, None] >> np.array([0, 2, 4, 6], dtype=np.uint8)) & 3).ravel(), minlength=4)
+        assert (seg > 0).all(), f"not every segment sampled: {seg}"
     # norm forward, backward on synthetic (y, rstd), chain fwd->bwd
     y_ref, r_ref = check_norm_fwd(c["norm"], dtype, xn[idx].cpu(), 1e-6, yn[idx], rstd[idx])
     check_norm_bwd(c["norm"], dtype, gn[idx].cpu(), dec(ys[idx].cpu(), dtype),
