@@ -323,11 +323,15 @@ int oracle_reswiglu2_bwd(const double *dh, const double *u, const double *a, con
 /* k-bit step activations: Eq. 14 with 2^k - 1 ReLUs  */
 /* (P:L353-362); derivative = 2^k-segment step (Prop. 4.1).          */
 /* code = #{i : x > c_i}; packed k bits per element, element j at bits       */
-/* k*j .. k*j+k-1 of the LSB-first stream, trailing bits zero.      */
+/* k*j .. k*j+k-1 of the LSB-first bit stream, trailing bits zero. */
+/* k = 1..4 ("k is the required bit number"; k bits per element,   */
+/* P:L371; "a larger k ... is also feasible").  For k = 3 a code    */
+/* straddles a byte boundary whenever k*j mod 8 > 5, so codes are written   */
+/* and read one bit at a time: bit b of code j is stream bit k*j + b.       */
 /* ------------------------------------------------------------------------ */
 int oracle_stepact_fwd(int kind, int k, const double *c, const double *x, int64_t n, double *y, uint8_t *codes)
 {
-    if (k != 1 && k != 2 && k != 4) return -1;
+    if (k < 1 || k > 4) return -1;
     int nt = (1 << k) - 1;
     int64_t nbytes = (n * k + 7) / 8;
     for (int64_t b = 0; b < nbytes; ++b) codes[b] = 0;
@@ -335,19 +339,23 @@ int oracle_stepact_fwd(int kind, int k, const double *c, const double *x, int64_
         y[j] = (kind == ORACLE_GELU) ? oracle_gelu(x[j]) : oracle_silu(x[j]);
         unsigned code = 0;
         for (int i = 0; i < nt; ++i) code += (unsigned)(x[j] > c[i]);
-        int64_t bit = (int64_t)k * j;
-        codes[bit / 8] |= (uint8_t)(code << (bit % 8));
+        for (int b = 0; b < k; ++b) {
+            int64_t bit = (int64_t)k * j + b;
+            codes[bit / 8] |= (uint8_t)(((code >> b) & 1u) << (bit % 8));
+        }
     }
     return 0;
 }
 
 int oracle_stepact_bwd(int k, const double *s, const uint8_t *codes, const double *dy, int64_t n, double *dx)
 {
-    if (k != 1 && k != 2 && k != 4) return -1;
-    unsigned mask = (1u << k) - 1u;
+    if (k < 1 || k > 4) return -1;
     for (int64_t j = 0; j < n; ++j) {
-        int64_t bit = (int64_t)k * j;
-        unsigned code = (codes[bit / 8] >> (bit % 8)) & mask;
+        unsigned code = 0;
+        for (int b = 0; b < k; ++b) {
+            int64_t bit = (int64_t)k * j + b;
+            code |= (unsigned)((codes[bit / 8] >> (bit % 8)) & 1u) << b;
+        }
         dx[j] = s[code] * dy[j];
     }
     return 0;

@@ -231,8 +231,18 @@ def _dbl(vals):
     return arr, ctypes.addressof(arr)
 
 
+def _check_table(fn: str, k: int, vals, want: int, what: str):
+    """The C ABI reads exactly `want` doubles: refuse any other length here,
+    before a short host array could be read past its end."""
+    if int(k) not in (1, 2, 3, 4):
+        raise ValueError(f"{fn}: k must be 1, 2, 3 or 4 (got {k})")
+    if len(vals) != want:
+        raise ValueError(f"{fn}: {what} needs exactly {want} entries for k = {k} (got {len(vals)})")
+
+
 def stepact_fwd(x, act: str, k: int, thresholds, y=None, codes=None, stream=None):
     """Forward of a k-bit step activation: (y = act(x), k-bit codes)."""
+    _check_table("stepact_fwd", k, thresholds, (1 << int(k)) - 1, "thresholds")
     _need(x, "x")
     n = x.numel()
     y = torch.empty_like(x) if y is None else _need(y, "y")
@@ -252,8 +262,11 @@ def stepact_fwd(x, act: str, k: int, thresholds, y=None, codes=None, stream=None
 
 def stepact_bwd(dy, codes, k: int, levels, dx=None, stream=None):
     """Backward of a k-bit step activation: dx = dy * levels[code]."""
+    _check_table("stepact_bwd", k, levels, 1 << int(k), "levels")
     _need(dy, "dy")
     _need(codes, "codes")
+    if codes.dtype != torch.uint8:
+        raise ValueError("stepact_bwd: codes must be uint8")
     n = dy.numel()
     dx = torch.empty_like(dy) if dx is None else _need(dx, "dx")
     if codes.numel() != codes_bytes_k(n, k) or dx.shape != dy.shape or dx.dtype != dy.dtype:

@@ -574,6 +574,47 @@ def test_stepact_k4_codes_are_searchsorted():
     assert np.array_equal(oracle.stepact_bwd(4, s, codes, dy), s[want] * dy)
 
 
+def _pack_bits(codes, k):
+    """Independent bit-stream packer: stream bit k*j + b = bit b of code j
+    (LSB first), built as one Python integer, then cut into bytes."""
+    acc = 0
+    for j, c in enumerate(codes):
+        acc |= int(c) << (k * j)
+    return np.frombuffer(acc.to_bytes((len(codes) * k + 7) // 8, "little"), dtype=np.uint8)
+
+
+def test_stepact_k3_hand_packed_stream():
+    """k = 3: codes 0..7 of x placed between thresholds 0.5 .. 6.5; the 24-bit
+    stream 111 110 101 100 011 010 001 000 (LSB first) is 0xFAC688, i.e. the
+    bytes 88 C6 FA -- codes 2 and 5 straddle byte boundaries."""
+    c = np.arange(7) + 0.5                                         # 0.5, 1.5, ..., 6.5
+    x = np.arange(8, dtype=np.float64)                             # code j for x = j
+    _, codes = oracle.stepact_fwd("gelu", 3, c, x)
+    assert codes.tolist() == [0x88, 0xC6, 0xFA]
+    s = np.arange(8) * 10.0
+    assert oracle.stepact_bwd(3, s, codes, np.ones(8)).tolist() == [0, 10, 20, 30, 40, 50, 60, 70]
+    # ragged tail: 3 elements = 9 bits -> 2 bytes, unused bits zero
+    _, c3 = oracle.stepact_fwd("gelu", 3, c, np.array([7.0, 7.0, 7.0]))
+    assert c3.tolist() == [0xFF, 0x01]
+
+
+def test_stepact_k3_codes_are_searchsorted():
+    rng = np.random.default_rng(17)
+    c = np.sort(rng.normal(size=7) * 3)
+    x = np.concatenate([rng.normal(size=3001) * 4, c, np.nextafter(c, np.inf), [np.nan, np.inf, -np.inf]])
+    _, codes = oracle.stepact_fwd("silu", 3, c, x)
+    want = np.searchsorted(c, x, side="left")                    # #{i : c_i < x}
+    want[np.isnan(x)] = 0                                         # NaN > c is false (R8)
+    assert np.array_equal(codes, _pack_bits(want, 3))
+    s = rng.normal(size=8)
+    dy = rng.normal(size=x.size)
+    assert np.array_equal(oracle.stepact_bwd(3, s, codes, dy), s[want] * dy)
+    for k in (1, 2, 4):                                           # the same packer agrees for byte-local k
+        cc = np.sort(rng.normal(size=(1 << k) - 1))
+        _, ck = oracle.stepact_fwd("silu", k, cc, x[:1000])
+        assert np.array_equal(ck, _pack_bits(np.searchsorted(cc, x[:1000], side="left"), k))
+
+
 def test_stepact_k2_equals_regelu2_and_resilu2():
     rng = np.random.default_rng(16)
     x = rng.normal(size=2001) * 5
