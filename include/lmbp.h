@@ -193,8 +193,10 @@ LMBP_API int reswiglu2_bwd(const void *dh, const void *up, const void *a, const 
  *           levels: HOST pointer to 2^k finite binary64 values.
  * codes: lmbp_codes_bytes_k(rows*cols, k) = ceil(n k / 8) bytes; element j
  *        at bits k*j .. k*j+k-1 of the LSB-first bit stream;
- *        trailing bits of the last byte written as 0.
- * k must be 1, 2 or 4 (else LMBP_ERR_TABLE, as for a malformed table).
+ *        trailing bits of the last byte written as 0.  For k = 3 a code
+ *        may straddle two bytes (every 8 elements from a multiple of 8 fill
+ *        exactly 3 bytes).
+ * k must be 1, 2, 3 or 4 (else LMBP_ERR_TABLE, as for a malformed table).
  * Layout, alignment (any; 16-byte aligned tensors take the vector path with
  * identical results), aliasing and the other errors as above.
  * ------------------------------------------------------------------------- */
@@ -224,7 +226,9 @@ LMBP_API int stepact_bwd(int k, const double *levels, const void *dy, const uint
  *   (on intervals of >= 12 panels the theta-independent outer pieces come
  *   from per-block prefix tables plus one partial panel each).
  * Errors: act / objective unknown -> LMBP_ERR_KIND; k outside 1..4 or
- *   n < 0 -> LMBP_ERR_SHAPE; eps not in (0, 1) -> LMBP_ERR_EPS; NULL pointer
+ *   n < 0 -> LMBP_ERR_SHAPE; eps not in (0, 1) -> LMBP_ERR_EPS (also for
+ *   lmbp_fit_anneal_vp when [A, B] spans more than 64 panels of length 2,
+ *   e.g. SiLU with eps < ~2.5e-14: its tables cannot hold them); NULL pointer
  *   with work to do -> LMBP_ERR_NULLPTR; bad annealing schedule (chains < 1,
  *   iters < 0, t0 / t1 / step0 / step1 not finite and > 0) -> LMBP_ERR_ARG;
  *   launch failure -> LMBP_ERR_CUDA.  Deterministic for a given seed.

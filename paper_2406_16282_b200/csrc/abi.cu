@@ -90,7 +90,7 @@ static int swiglu_bwd_entry(const void *dh, const void *u, const void *a, const 
   return status_of(swiglu_bwd(dtype, dh, u, a, codes, dg, du, rows * cols, static_cast<cudaStream_t>(stream)));
 }
 
-static bool k_ok(int k) { return k == 1 || k == 2 || k == 4; }
+static bool k_ok(int k) { return k >= 1 && k <= 4; }
 
 // Round a binary64 threshold toward -inf into binary32 (reading R2).
 static float rd32(double c) {
@@ -279,6 +279,10 @@ static int fit_anneal_entry(bool vp, int act, int objective, int k, double eps, 
       !lmbp::pos_finite(step1))
     return LMBP_ERR_ARG;
   if (!chain_theta || !chain_J || !best) return LMBP_ERR_NULLPTR;
+  // the projected anneal integrates the weights' normal equations from
+  // per-CTA tables of ceil((B - A) / panel) cells; a tail tolerance so small
+  // that [A, B] needs more cells than the tables hold cannot be served
+  if (vp && std::ceil((s.B - s.A) / s.panel) > lmbp::kFitMaxCells) return LMBP_ERR_EPS;
   lmbp::AnnealCfg a{chains, iters, seed, t0, t1, step0, step1};
   const cudaStream_t cs = static_cast<cudaStream_t>(stream);
   return lmbp::status_of(vp ? lmbp::fit_anneal_vp(s, k, a, init, chain_theta, chain_J, best, cs)

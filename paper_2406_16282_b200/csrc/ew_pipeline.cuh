@@ -13,8 +13,9 @@
 // An Op supplies the shape and the per-vector work:
 //   static constexpr int W, U, S;   consumer warps, vectors per lane per tile, stages
 //   static constexpr int kIn;       input streams (1..3)
-//   static constexpr int kCodeIn;   bytes of packed codes read per vector (0, 1, 2)
-//   static constexpr int kCodeOut;  // bytes of packed codes written per vector (0, 1, 2)
+//   static constexpr int kCodeIn;   bytes of packed codes read per vector (0 .. 4)
+//   static constexpr int kCodeOut;  bytes of packed codes written per vector (0 .. 4; 3 = k = 3
+//                                   codes of 8 16-bit elements, written / read as single bytes)
 //   using Params = ...;            optional, a struct derived from EwParams (default EwParams)
 //   __device__ static uint32_t apply(const uint4 (&v)[kIn], uint32_t code, int64_t i, const Params &p);
 //       -> the code word of vector i (ignored when kCodeOut == 0)
@@ -66,13 +67,19 @@ template <class Op> struct EwShape {
 template <int kCodeOut>
 __device__ __forceinline__ void put_code(uint8_t *base, int64_t i, uint32_t c) {
   if constexpr (kCodeOut == 4) reinterpret_cast<uint32_t *>(base)[i] = c;
-  else if constexpr (kCodeOut == 2) reinterpret_cast<uint16_t *>(base)[i] = (uint16_t)c;
+  else if constexpr (kCodeOut == 3) {
+    base[3 * i] = (uint8_t)c;
+    base[3 * i + 1] = (uint8_t)(c >> 8);
+    base[3 * i + 2] = (uint8_t)(c >> 16);
+  } else if constexpr (kCodeOut == 2) reinterpret_cast<uint16_t *>(base)[i] = (uint16_t)c;
   else if constexpr (kCodeOut == 1) base[i] = (uint8_t)c;
 }
 
 template <int kCodeIn>
 __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
   if constexpr (kCodeIn == 4) return reinterpret_cast<const uint32_t *>(base)[i];
+  else if constexpr (kCodeIn == 3)
+    return (uint32_t)base[3 * i] | ((uint32_t)base[3 * i + 1] << 8) | ((uint32_t)base[3 * i + 2] << 16);
   else if constexpr (kCodeIn == 2) return reinterpret_cast<const uint16_t *>(base)[i];
   else if constexpr (kCodeIn == 1) return base[i];
   else return 0u;

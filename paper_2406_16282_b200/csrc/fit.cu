@@ -118,7 +118,7 @@ __device__ __forceinline__ double integrate_piece(const FitSpec &s, double l, do
 // (16-point Gauss-Legendre per cell, prefix sums), and an evaluation adds one
 // partial-cell panel per tail -- for SiLU (B - A = 76) that replaces ~35 of
 // ~41 panels per objective.
-constexpr int kMaxCells = 64;
+constexpr int kMaxCells = kFitMaxCells;
 constexpr int kMinCells = 12;
 struct FitTables {
   int n;                                       // cells; 0 = no table (too many cells)

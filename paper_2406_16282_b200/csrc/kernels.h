@@ -36,6 +36,9 @@ struct FitSpec {
   double A, B;   // truncated interval (App. E tail bounds)
   double panel;  // longest Gauss-Legendre panel
 };
+// Cells of the per-CTA prefix tables (panel grid over [A, B]); the
+// variable-projection anneal needs them, so it refuses a wider interval.
+constexpr int kFitMaxCells = 64;
 struct AnnealCfg {
   int64_t chains, iters;
   uint64_t seed;

@@ -571,7 +571,7 @@ struct RowTmaPlan {
 
 static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   RowTmaPlan p{false, 0, 0, 0, 0};
-  if (nvec < 256 || nvec > 16 * 32 * 8) return p;
+  if (nvec < 256 || nvec > 16 * 32 * 4) return p;
 #ifndef LMBP_ROW_VAIM
 #define LMBP_ROW_VAIM 4
 #endif
@@ -581,7 +581,10 @@ static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   int warps = (int)((nvec + LMBP_ROW_VAIM * 32 - 1) / (LMBP_ROW_VAIM * 32));  // aim for 4 vectors per thread
   if (warps > 16) warps = 16;
   const int V = (int)((nvec + warps * 32 - 1) / (warps * 32));
-  if (V > 8) return p;
+  // 17 warps under __launch_bounds__(544) leave ~120 registers per thread:
+  // V > 4 would spill (ptxas), so wider rows (> 2048 vectors, H > 16384 at
+  // 16 bits) take the per-warp ring instead.
+  if (V > 4) return p;
   const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
   int stages = (int)std::min<size_t>(4, (size_t)(LMBP_ROW_STAGE_KB * 1024) / stage);
   if (stages < 2) stages = 2;
@@ -620,11 +623,7 @@ static cudaError_t launch_row_tma(const RowTmaPlan &rp, const void *a, const voi
     case 1: return launch_row_tma_v<T, NORM, kFwd, 1>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
     case 2: return launch_row_tma_v<T, NORM, kFwd, 2>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
     case 3: return launch_row_tma_v<T, NORM, kFwd, 3>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 4: return launch_row_tma_v<T, NORM, kFwd, 4>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 5: return launch_row_tma_v<T, NORM, kFwd, 5>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 6: return launch_row_tma_v<T, NORM, kFwd, 6>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 7: return launch_row_tma_v<T, NORM, kFwd, 7>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    default: return launch_row_tma_v<T, NORM, kFwd, 8>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    default: return launch_row_tma_v<T, NORM, kFwd, 4>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
   }
 }
 
@@ -786,11 +785,13 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
   return p;
 }
 
-// Resident CTAs per SM for (kernel, threads); cached per kernel instantiation
-// and block size (a benign race: every writer stores the same value).
-template <typename K>
-static int occupancy_of(K kernel, int threads) {
+// Resident CTAs per SM for (kernel, threads).  The kernel is a template
+// argument, so every kernel instantiation has its own cache, slotted by block
+// size (a benign race: every writer stores the same value).
+template <auto Kern>
+static int occupancy_of(int threads) {
   static std::atomic<int> cache[33];  // zero-initialised (static storage)
+  const auto kernel = Kern;
   const int slot = threads >> 5;
   if (slot < 33) {
     const int c = cache[slot].load(std::memory_order_relaxed);
@@ -822,7 +823,7 @@ static void fwd_v(const RowPlan &p, const void *x, void *y, float *rstd, int64_t
                   cudaStream_t s) {
   auto k = norm_fwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
-  const int occ = occupancy_of(k, threads);
+  const int occ = occupancy_of<norm_fwd_vec<T, NORM, V, W>>(threads);
   launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, V <= 4, reinterpret_cast<const uint4 *>(x),
               reinterpret_cast<uint4 *>(y), rstd, rows, p.nvec, (int)cols, eps);
 }
@@ -832,7 +833,7 @@ static void bwd_v(const RowPlan &p, const void *dy, const void *y, const float *
                   int64_t cols, cudaStream_t s) {
   auto k = norm_bwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
-  const int occ = occupancy_of(k, threads);
+  const int occ = occupancy_of<norm_bwd_vec<T, NORM, V, W>>(threads);
   launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, true, reinterpret_cast<const uint4 *>(dy),
               reinterpret_cast<const uint4 *>(y), rstd, reinterpret_cast<uint4 *>(dx), rows, p.nvec, (int)cols);
 }
@@ -860,7 +861,7 @@ static cudaError_t norm_fwd_t(const void *x, void *y, float *rstd, int64_t rows,
   }
   if (!p.vec) {
     auto k = norm_fwd_scalar<T, NORM>;
-    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), true, reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
+    launch_rows(k, rows, 1, 256, s, occupancy_of<norm_fwd_scalar<T, NORM>>(256), true, reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y),
                 rstd, rows, cols, eps);
     return cudaGetLastError();
   }
@@ -913,7 +914,7 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
   }
   if (!p.vec) {
     auto k = norm_bwd_scalar<T, NORM>;
-    launch_rows(k, rows, 1, 256, s, occupancy_of(k, 256), true, reinterpret_cast<const T *>(dy),
+    launch_rows(k, rows, 1, 256, s, occupancy_of<norm_bwd_scalar<T, NORM>>(256), true, reinterpret_cast<const T *>(dy),
                 reinterpret_cast<const T *>(y), rstd, reinterpret_cast<T *>(dx), rows, cols);
     return cudaGetLastError();
   }

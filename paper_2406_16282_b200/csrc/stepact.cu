@@ -6,12 +6,14 @@
 // dh~ (Prop. 4.1), so k bits per element are stored (P:L362,
 // "k is the required bit number").  k = 2 with the published tables is
 // ReGELU2 / ReSiLU2 (bitwise identical to regelu2_* / resilu2_*, tested);
-// other tables cover ReGELU2-d (App. I) and k = 1 / 4 variants
-// ("setting a larger k ... is also feasible").
+// other tables cover ReGELU2-d (App. I) and k = 1 / 3 / 4
+// variants ("setting a larger k ... is also feasible").
 //
 // Packing: element j occupies bits k*j .. k*j + k - 1 of the flat
-// LSB-first bit stream, i.e. byte (k*j) / 8 at shift (k*j) % 8 (k | 8).
-// A thread owns groups of 8 elements = k bytes of codes.
+// LSB-first bit stream.  Any 8 consecutive elements starting at a multiple of
+// 8 fill exactly k whole bytes, so a thread (or a 16-byte vector of 8 16-bit
+// elements) owns k bytes of codes; for k = 3 a single code may straddle two
+// of those bytes (handled by building the group's 24-bit word first).
 #include "act_math.cuh"
 #include "common.cuh"
 #include "ew_pipeline.cuh"
@@ -45,6 +47,17 @@ __device__ __forceinline__ uint32_t step_code(float x, const float *thr) {
 #pragma unroll
   for (int i = 0; i < (1 << K) - 1; ++i) c += (uint32_t)(x > thr[i]);
   return c;
+}
+
+// Code of element j read from the packed stream, for any k <= 4 (a k = 3
+// code straddles a byte boundary when (3 j) % 8 > 5; the second byte exists
+// then because the code's bits lie inside the stream).
+template <int K>
+__device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int64_t j) {
+  const int64_t bit = (int64_t)K * j;
+  uint32_t w = codes[bit >> 3];
+  if ((bit & 7) + K > 8) w |= (uint32_t)codes[(bit >> 3) + 1] << 8;
+  return (w >> (bit & 7)) & ((1u << K) - 1u);
 }
 
 template <typename T>
@@ -125,19 +138,16 @@ __global__ void __launch_bounds__(256) stepact_bwd_k(const T *dy, const uint8_t 
     store8<T>(dx, g, vec, f);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int64_t j = groups * 8; j < n; ++j) {
-      const int64_t bit = K * j;
-      const uint32_t c = (codes[bit >> 3] >> (bit & 7)) & kMask;
-      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), lvl[c]));
-    }
+    for (int64_t j = groups * 8; j < n; ++j)
+      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), lvl[code_at<K>(codes, j)]));
   }
 }
 
 // ---------------------------------------------------------------------------
 // TMA/CLC pipeline path (ew_pipeline.cuh): one 16-byte vector of kVec
 // elements yields kVec k bits = kVec k / 8 whole bytes of codes (needs
-// kVec k >= 8: every case except fp32 with k = 1, which keeps the simple
-// kernel).  Same per-element arithmetic as the simple kernel -> bitwise equal.
+// kVec k to be a multiple of 8: every case except fp32 with k = 1 or k = 3,
+// which keep the simple kernel).  Same per-element arithmetic as the simple kernel -> bitwise equal.
 // ---------------------------------------------------------------------------
 struct StepEwParams : EwParams {
   StepTable tab;  // runtime step table
@@ -283,14 +293,10 @@ struct StepBwdOp {
     return 0u;
   }
   __device__ static void tail(const StepEwParams &p) {
-    constexpr uint32_t kMask = (1u << K) - 1u;
     const T *dy = reinterpret_cast<const T *>(p.in[0]);
     T *dx = reinterpret_cast<T *>(p.out[0]);
-    for (int64_t j = p.nvec * kVecT; j < p.n; ++j) {
-      const int64_t bit = K * j;
-      const uint32_t c = (p.codes_in[bit >> 3] >> (bit & 7)) & kMask;
-      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), p.tab.lvl[c]));
-    }
+    for (int64_t j = p.nvec * kVecT; j < p.n; ++j)
+      dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), p.tab.lvl[code_at<K>(p.codes_in, j)]));
   }
 };
 
@@ -304,7 +310,7 @@ static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t
                                  cudaStream_t s) {
   constexpr bool kPrecise = std::is_same<T, float>::value;
   const bool vec = (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
-  if constexpr (Traits<T>::kVec * K >= 8) {
+  if constexpr ((Traits<T>::kVec * K) % 8 == 0) {
     if (vec && (uintptr_t)codes % 16 == 0) {
       StepEwParams p{};
       p.in[0] = reinterpret_cast<const uint4 *>(x);
@@ -325,7 +331,7 @@ template <typename T, int K>
 static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx, int64_t n, const StepTable &tab,
                                  cudaStream_t s) {
   const bool vec = (uintptr_t)dy % 16 == 0 && (uintptr_t)dx % 16 == 0;
-  if constexpr (Traits<T>::kVec * K >= 8) {
+  if constexpr ((Traits<T>::kVec * K) % 8 == 0) {
     if (vec && (uintptr_t)codes % 16 == 0) {
       StepEwParams p{};
       p.in[0] = reinterpret_cast<const uint4 *>(dy);
@@ -346,6 +352,7 @@ template <typename T, int A>
 static cudaError_t fwd_k(int k, const void *x, void *y, uint8_t *codes, int64_t n, const StepTable &t, cudaStream_t s) {
   if (k == 1) return stepact_fwd_t<T, A, 1>(x, y, codes, n, t, s);
   if (k == 2) return stepact_fwd_t<T, A, 2>(x, y, codes, n, t, s);
+  if (k == 3) return stepact_fwd_t<T, A, 3>(x, y, codes, n, t, s);
   return stepact_fwd_t<T, A, 4>(x, y, codes, n, t, s);
 }
 
@@ -354,6 +361,7 @@ static cudaError_t bwd_k(int k, const void *dy, const uint8_t *codes, void *dx, 
                          cudaStream_t s) {
   if (k == 1) return stepact_bwd_t<T, 1>(dy, codes, dx, n, t, s);
   if (k == 2) return stepact_bwd_t<T, 2>(dy, codes, dx, n, t, s);
+  if (k == 3) return stepact_bwd_t<T, 3>(dy, codes, dx, n, t, s);
   return stepact_bwd_t<T, 4>(dy, codes, dx, n, t, s);
 }
 

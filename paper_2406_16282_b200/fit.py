@@ -48,8 +48,16 @@ def fit(act: str, k: int = 2, objective: str = "h", refine_iters: int = 40, proj
     the best refined point taken.  projected (default) anneals only the
     thresholds with least-squares weights (lmbp_fit_anneal_vp): the same k = 2
     optimum 2-3x sooner, and the only variant that converges for k >= 3;
-    projected=False anneals all 2m - 1 parameters (lmbp_fit_anneal)."""
-    best, chain_theta, chain_J = ops.fit_anneal(act, k=k, objective=objective, projected=projected, **anneal_kw)
+    projected=False anneals all 2m - 1 parameters (lmbp_fit_anneal); it is
+    also taken when the projected anneal refuses the interval (a tail
+    tolerance so small that [A, B] exceeds its tables: LMBP_ERR_EPS)."""
+    from ._lib import LMBP_ERR_EPS, LmbpError
+    try:
+        best, chain_theta, chain_J = ops.fit_anneal(act, k=k, objective=objective, projected=projected, **anneal_kw)
+    except LmbpError as e:
+        if not (projected and e.status == LMBP_ERR_EPS and anneal_kw.get("eps", 1e-8) > 0):
+            raise
+        best, chain_theta, chain_J = ops.fit_anneal(act, k=k, objective=objective, projected=False, **anneal_kw)
     if refine_iters > 0:
         best, _, _ = ops.fit_refine(chain_theta, act, k=k, objective=objective,
                                     eps=anneal_kw.get("eps", 1e-8), iters=refine_iters)

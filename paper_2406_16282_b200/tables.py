@@ -14,5 +14,23 @@ REGELU2_D = dict(act="gelu", k=2, a=(0.32465931184406527, 0.34812875668739607),
 
 
 def levels(table):
-    a1, a2 = table["a"]
-    return (0.0, a1, a1 + a2, 1.0)
+    """s_j = sum of the first j weights of Eq. 14, the last
+    weight being 1 - sum(a), so s_0 = 0 and s_m = 1 exactly; for k = 2 this is
+    (0, a1, a1 + a2, 1).  Requires the thresholds sorted increasingly (the
+    fitter's canonical order, DESIGN F5)."""
+    a = [float(v) for v in table["a"]]
+    out, acc = [0.0], 0.0
+    for w in a:
+        acc += w
+        out.append(acc)
+    out.append(1.0)
+    return tuple(out)
+
+
+def from_fit(f):
+    """Step table of a fitter result (fit.Fit: a = m - 1 weights, c = m
+    thresholds, m = 2^k - 1, pairs sorted by c)."""
+    c = [float(v) for v in f.c]
+    if sorted(c) != c:
+        raise ValueError("fitter thresholds must be increasing")
+    return dict(act=f.act, k=f.k, a=tuple(f.a), c=tuple(c))

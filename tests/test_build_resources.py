@@ -60,3 +60,17 @@ def test_kbit_forward_register_budget():
     for m in re.finditer(r"Function properties for (\S+)\n.*?(\d+) bytes spill stores", text):
         if "StepFwdOp" in demangle([m.group(1)])[m.group(1)]:
             assert int(m.group(2)) == 0, m.group(1)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "norm.ptxas.log")), reason="no build logs")
+def test_norm_row_pipeline_does_not_spill():
+    """norm_row_tma runs 544-thread CTAs (~120 registers per thread): only
+    V <= 4 instantiations exist and none spills."""
+    text = open(os.path.join(OBJ, "norm.ptxas.log")).read()
+    seen = 0
+    for m in re.finditer(r"Function properties for (\S+)\n.*?(\d+) bytes spill stores", text):
+        name = demangle([m.group(1)])[m.group(1)]
+        if "norm_row_tma" in name:
+            seen += 1
+            assert int(m.group(2)) == 0, name
+    assert seen > 0

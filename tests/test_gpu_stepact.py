@@ -1,6 +1,6 @@
 """GPU parity for the table-driven k-bit step activations (SURVEY 8(f)
 NEXT #3): k = 2 with the published tables is bitwise identical to the
-specialised regelu2/resilu2 kernels; k = 1, 2 (ReGELU2-d), 4 against the
+specialised regelu2/resilu2 kernels; k = 1, 2 (ReGELU2-d), 3, 4 against the
 oracle (codes bytewise, y within tolerance, dx bitwise to the contract)."""
 import numpy as np
 import pytest
@@ -38,11 +38,12 @@ def _tables(k, rng):
     if k == 2:
         c, s = oracle.regelu2d_table()
         return list(c), list(s)
-    c = sorted(rng.normal(size=15) * 3)
-    return c, list(rng.normal(size=16))
+    m = (1 << k) - 1
+    c = sorted(rng.normal(size=m) * 3)
+    return c, list(rng.normal(size=m + 1))
 
 
-@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 @pytest.mark.parametrize("shape", [(1, 5), (7, 33), (64, 3072)])
 def test_stepact_vs_oracle(k, dtype, shape):
@@ -70,7 +71,7 @@ def test_stepact_bad_tables():
         P.stepact_fwd(x, "gelu", 2, [0.0, float("nan"), 2.0])
 
 
-@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 def test_stepact_paths_bitwise(k, dtype):
     """TMA pipeline path (aligned) == simple kernel path (misaligned codes)."""
@@ -89,29 +90,56 @@ def test_stepact_paths_bitwise(k, dtype):
     assert st(y0).tobytes() == st(y1).tobytes() and st(dx0).tobytes() == st(dx1).tobytes()
 
 
+@pytest.mark.parametrize("k", [3, 4])
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
-def test_stepact_k4_full_size_sampled(cfg):
+def test_stepact_full_size_sampled(cfg, k):
     """k = 4 at the BASELINE config's full activation size (TMA/CLC pipeline,
     binary-search packed compares, shared-memory level table), sampled rows
     against the oracle: codes bytewise, y within tolerance, dx bitwise."""
     from test_gpu_parity import sample_rows
     c = synth.CONFIGS[cfg]
     R, F, dtype = c["R"], c["F"], c["dtype"]
-    thr = [-3.0 + 0.4 * i for i in range(15)]
-    lv = [(-1) ** i * i / 15 for i in range(16)]
-    x = synth.act_input(R, F, dtype, device=DEV)
+    m = (1 << k) - 1
+    thr = [-3.0 + 6.0 * i / (m - 1) for i in range(m)]
+    lv = [(-1) ** i * i / m for i in range(m + 1)]
+    x = synth.act_input(R, F, dtype, device=DEV, mode="coverage")
     dy = synth.grad_input(R, F, dtype, device=DEV)
-    y, codes = P.stepact_fwd(x, c["act"], 4, thr)
-    dx = P.stepact_bwd(dy, codes, 4, lv)
+    y, codes = P.stepact_fwd(x, c["act"], k, thr)
+    dx = P.stepact_bwd(dy, codes, k, lv)
     torch.cuda.synchronize()
     rows = sample_rows(R)
     idx = torch.tensor(rows, device=DEV)
-    assert F % 2 == 0
-    cb = codes.view(R, F // 2)[idx].cpu().numpy().reshape(-1)
+    assert (F * k) % 8 == 0                                     # a row's codes are whole bytes
+    cb = codes.view(R, F * k // 8)[idx].cpu().numpy().reshape(-1)
     xs = x[idx].cpu()
-    y_ref, c_ref = oracle.stepact_fwd(c["act"], 4, thr, dec(xs, dtype))
+    y_ref, c_ref = oracle.stepact_fwd(c["act"], k, thr, dec(xs, dtype))
     assert np.array_equal(cb, c_ref)
     yr = y_ref.reshape(-1)
     assert np.all(np.abs(dec(y[idx].cpu(), dtype).reshape(-1) - yr) <= RTOL[dtype] * np.abs(yr) + ATOL[dtype])
-    want = oracle.stepact_bwd_contract(4, lv, c_ref, st(dy[idx].cpu()), dtype)
+    want = oracle.stepact_bwd_contract(k, lv, c_ref, st(dy[idx].cpu()), dtype)
     assert np.array_equal(bits(st(dx[idx].cpu())), bits(want))
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_stepact_k3_with_fitted_table(act, dtype):
+    """The fitter's k = 3 solution (App. E objective, 7 ReLUs) fed straight
+    into the k = 3 kernels: codes bytewise and dx bitwise against the oracle
+    run with the same table; the table's levels are the Eq. 14 slopes."""
+    from paper_2406_16282_b200 import fit as gfit
+    f = gfit.fit(act, k=3, chains=2048, iters=800, refine_iters=10)
+    tab = tables.from_fit(f)
+    lv = tables.levels(tab)
+    assert len(tab["c"]) == 7 and len(lv) == 8 and lv[0] == 0.0 and lv[-1] == 1.0
+    R, F = 64, 3072 + 8 * 3 + 5                                 # ragged: a code straddles the last bytes
+    x = synth.act_input(R, F, dtype, mode="coverage")
+    dy = synth.grad_input(R, F, dtype)
+    y, codes = P.stepact_fwd(x.to(DEV), act, 3, tab["c"])
+    dx = P.stepact_bwd(dy.to(DEV), codes, 3, lv)
+    torch.cuda.synchronize()
+    y_ref, c_ref = oracle.stepact_fwd(act, 3, tab["c"], dec(x, dtype))
+    assert np.array_equal(codes.cpu().numpy(), c_ref)
+    want = oracle.stepact_bwd_contract(3, lv, c_ref, st(dy), dtype)
+    assert np.array_equal(bits(st(dx)), bits(want))
+    seg = np.bincount(np.searchsorted(np.array(tab["c"]), dec(x, dtype).reshape(-1), side="left"), minlength=8)
+    assert (seg > 0).all(), seg
