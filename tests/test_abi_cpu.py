@@ -102,7 +102,7 @@ def test_validation_without_device_work():
     good = (ctypes.c_double * 3)(-1.0, 0.0, 1.0)
     bad = (ctypes.c_double * 3)(1.0, 0.0, 2.0)
     lv = (ctypes.c_double * 4)(0.0, 0.1, 0.9, 1.0)
-    assert L.stepact_fwd(0, 3, ctypes.addressof(good), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
+    assert L.stepact_fwd(0, 5, ctypes.addressof(good), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
     assert L.stepact_fwd(0, 2, ctypes.addressof(bad), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
     assert L.stepact_fwd(9, 2, ctypes.addressof(good), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_KIND
     assert L.stepact_fwd(0, 2, None, fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_NULLPTR
@@ -110,8 +110,8 @@ def test_validation_without_device_work():
     assert L.stepact_bwd(2, ctypes.addressof(lv), fake, fake, fake, -1, 4, 0, None) == S.LMBP_ERR_SHAPE
     assert L.stepact_bwd(5, ctypes.addressof(lv), fake, fake, fake, 2, 4, 0, None) == S.LMBP_ERR_TABLE
     assert L.stepact_bwd(2, ctypes.addressof(lv), None, None, None, 0, 4, 0, None) == S.LMBP_OK
-    for k, n in ((1, 9), (2, 9), (4, 9), (3, 9), (2, 0)):
-        assert L.lmbp_codes_bytes_k(n, k) == ((n * k + 7) // 8 if k in (1, 2, 4) else 0)
+    for k, n in ((1, 9), (2, 9), (4, 9), (3, 9), (5, 9), (2, 0)):
+        assert L.lmbp_codes_bytes_k(n, k) == ((n * k + 7) // 8 if k in (1, 2, 3, 4) else 0)
     t = (ctypes.c_float * 4)()
     assert L.lmbp_step_table(5, ctypes.addressof(t), ctypes.addressof(t)) == S.LMBP_ERR_KIND
     assert L.lmbp_step_table(0, None, ctypes.addressof(t)) == S.LMBP_ERR_NULLPTR
@@ -214,3 +214,20 @@ int main(void) {
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stderr)
     assert r.stdout.startswith("LMBP_ERR_SHAPE")
+
+
+def test_stepact_binding_refuses_wrong_table_lengths():
+    """The C ABI reads exactly 2^k - 1 thresholds / 2^k levels from the host
+    pointer: the binding must refuse any other length before the call
+    (ADVICE r1), and non-uint8 codes."""
+    import torch
+    from paper_2406_16282_b200 import ops
+    x = torch.zeros(4, 8)
+    with pytest.raises(ValueError, match="exactly 15"):
+        ops.stepact_fwd(x, "gelu", 4, [-1.0, 0.0, 1.0])         # the 3 published thresholds with k = 4
+    with pytest.raises(ValueError, match="exactly 3"):
+        ops.stepact_fwd(x, "gelu", 2, [-1.0, 0.0, 1.0, 2.0])
+    with pytest.raises(ValueError, match="exactly 8"):
+        ops.stepact_bwd(x, torch.zeros(12, dtype=torch.uint8), 3, [0.0] * 7)
+    with pytest.raises(ValueError, match="k must be"):
+        ops.stepact_fwd(x, "gelu", 5, [0.0] * 31)
