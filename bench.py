@@ -560,24 +560,37 @@ def fitter_section(stream, cpu=True, chains=148 * 3 * 128, iters=1000, n_obj=148
     return out
 
 
-def block_section(cfg, R, dev):
-    """activation bytes an FFN half-block keeps for
-    backward (measured with saved_tensors_hooks, storage-deduplicated,
-    parameters excluded) -- exact reference (affine norm in fp32, exact
-    GELU/SiLU) vs ours (merged affine, MS norm, ReGELU2 / fused ReSwiGLU2) at
-    the config's shape; unit = one [R, H] 16-bit tensor (Fig. 2's unit)."""
-    from paper_2406_16282_b200.blocks import LlamaMLP, ViTMLP, activation_bytes
-    cls = ViTMLP if cfg["act"] == "gelu" else LlamaMLP
-    dt = synth.TORCH_DTYPES[cfg["dtype"]]
-    blk = cls(cfg["H"], cfg["F"], dtype=dt, device=dev)
-    x = synth.norm_input(R, cfg["H"], cfg["dtype"], device=dev).requires_grad_(True)
-    exact = activation_bytes(blk, x)
-    ours = activation_bytes(blk.to_ours(), x)
-    unit = R * cfg["H"] * 2
-    torch.cuda.synchronize()
-    return {"block": cls.__name__, "rows": R, "exact_bytes": exact, "ours_bytes": ours,
-            "saved_fraction": round(1 - ours / exact, 4), "exact_units": round(exact / unit, 3),
-            "ours_units": round(ours / unit, 3)}
+def block_section(cfg, dev, tunings=("full", "lora_qv", "lora_all", "lora_fa_all", "frozen_ffn")):
+    """activation bytes a whole transformer block
+    (attention + FFN, the config's model dimensions and batch) keeps for
+    backward, measured with saved_tensors_hooks (storage-deduplicated,
+    parameters excluded), exact (affine norms in fp32 as under AMP, exact
+    GELU / SiLU) vs ours (merged affine, MS norms, ReGELU2 / fused ReSwiGLU2),
+    per fine-tuning regime; unit = one [b, n, c] 16-bit tensor (Fig. 5/6).
+    Where no consumer of a norm keeps its input (frozen / LoRA-FA; Prop. 5.1
+    condition 3 fails) the MS norm shares nothing."""
+    from paper_2406_16282_b200.blocks import Block, activation_bytes, unit_model
+    arch = "vit" if cfg["act"] == "gelu" else "llama"
+    dt = synth.TORCH_DTYPES[cfg["dtype"]] if cfg["dtype"] != "f32" else torch.bfloat16
+    b, n, c, h = cfg["batch"], cfg["seq"], cfg["H"], cfg["F"]
+    unit = b * n * c * 2
+    x = synth.norm_input(b * n, c, "bf16", device=dev).view(b, n, c).requires_grad_(True)
+    out = {"arch": arch, "shape": {"batch": b, "seq": n, "hidden": c, "ffn": h, "heads": cfg["heads"]},
+           "unit_bytes": unit, "decoded_model_full_tuning": {k: round(v, 4) for k, v in unit_model(arch, h / c).items()},
+           "model_note": "torch SDPA returns [b, n, h, d]: the out-projection's saved input is the attention output "
+                         "itself, one unit below the model's separate kernels", "tunings": {}}
+    for t in tunings:
+        blk = Block(arch, c, h, cfg["heads"], tuning=t, dtype=dt, device=dev)
+        te, pe = activation_bytes(blk, x, by_module=True)
+        to, po = activation_bytes(blk.to_ours(), x, by_module=True)
+        out["tunings"][t] = {"exact_units": round(te / unit, 4), "ours_units": round(to / unit, 4),
+                             "saved_fraction": round(1 - to / te, 4), "exact_bytes": te, "ours_bytes": to,
+                             "norm_shared": [blk.norm_shared(1), blk.norm_shared(2)],
+                             "per_module_units": {k: [round(pe.get(k, 0) / unit, 4), round(po.get(k, 0) / unit, 4)]
+                                                  for k in sorted(set(pe) | set(po))}}
+        del blk
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -851,7 +864,7 @@ def main(argv=None):
     assert all(sum(rwb[k]) == nbytes[k] for k in kernels)
     rw_model = rw_model_section(x, dy, dx, y, flush, flush_sink, stream, kern, rwb)
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
-    block = block_section(cfg, R, dev) if rank == 0 else None
+    block = block_section(cfg, dev) if rank == 0 else None
     step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink, peak)
     fitter = fitter_section(stream, cpu=(world == 1 and not args.no_cpu_baseline)) if (
         rank == 0 and not args.no_fitter) else None

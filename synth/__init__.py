@@ -36,19 +36,19 @@ ELEM_BYTES = {"f32": 4, "bf16": 2, "f16": 2}
 
 # name -> shapes.  R = tokens, F = activation width, H = normalised width.
 CONFIGS = {
-    "c1": dict(R=2 * 197, F=3072, H=768, dtype="f32", act="gelu", norm="ln",
+    "c1": dict(R=2 * 197, F=3072, H=768, dtype="f32", act="gelu", norm="ln", batch=2, seq=197, heads=12,
                desc="single ViT-B block slice: ReGELU2 on 2x197x3072 + MS-LN on 2x197x768, fp32",
                bj_index=0),
-    "c2": dict(R=64 * 197, F=3072, H=768, dtype="bf16", act="gelu", norm="ln",
+    "c2": dict(R=64 * 197, F=3072, H=768, dtype="bf16", act="gelu", norm="ln", batch=64, seq=197, heads=12,
                desc="ViT-B/16 LoRA: batch 64, 197 tokens, hidden 768, MLP 3072, bf16",
                bj_index=1),
-    "c3": dict(R=32 * 512, F=3072, H=768, dtype="f32", act="gelu", norm="ln",
+    "c3": dict(R=32 * 512, F=3072, H=768, dtype="f32", act="gelu", norm="ln", batch=32, seq=512, heads=12,
                desc="RoBERTa-base: batch 32, seq 512, hidden 768, FFN 3072 (fp32, P:L734)",
                bj_index=2),
-    "c4": dict(R=4 * 2048, F=11008, H=4096, dtype="bf16", act="silu", norm="rms",
+    "c4": dict(R=4 * 2048, F=11008, H=4096, dtype="bf16", act="silu", norm="rms", batch=4, seq=2048, heads=32,
                desc="LLaMA-7B: batch 4, seq 2048, hidden 4096, FFN 11008, ReSiLU2 gate + MS-RMSNorm, bf16",
                bj_index=3),
-    "c5": dict(R=8 * 4096, F=13824, H=5120, dtype="bf16", act="silu", norm="rms",
+    "c5": dict(R=8 * 4096, F=13824, H=5120, dtype="bf16", act="silu", norm="rms", batch=8, seq=4096, heads=40,
                desc="LLaMA-13B: batch 8, seq 4096, hidden 5120, FFN 13824, ReSiLU2 + MS-RMSNorm, bf16",
                bj_index=4),
 }

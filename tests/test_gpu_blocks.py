@@ -1,55 +1,195 @@
-"""Block-level integration: affine merge + MS norms +
-ReGELU2 / ReSwiGLU2 inside ViT / LLaMA FFN half-blocks.  The forward is
-unchanged, the memory-sharing backward is exact, and the
-activation memory kept for backward matches the analytic count byte for byte."""
+"""Block-level integration: whole ViT / LLaMA blocks
+(attention + FFN) under the paper's fine-tuning regimes, exact vs ours.
+
+* saved bytes per module, to the byte, for every regime -- including the
+  regimes where Prop. 5.1 condition 3 fails (frozen / LoRA-FA consumers,
+  P:L452) and the MS norm therefore shares nothing;
+* the block's MS-norm outputs are bytewise those of msln_fwd / msrms_fwd on the
+  same input, its packed codes bytewise the oracle's, and the norm backward
+  inside the block obeys the SURVEY 8(c) elementwise bound against the
+  oracle's Alg. 2 / Alg. 3 backward on the gradient the block delivered;
+* the merged block (affine folded, MS norms, exact activation) reproduces the
+  exact block's input gradient elementwise (fp32).
+"""
+import numpy as np
 import pytest
 import torch
 
+import oracle
 import synth
 import paper_2406_16282_b200 as P
-from paper_2406_16282_b200.blocks import LlamaMLP, ViTMLP, activation_bytes
+from paper_2406_16282_b200.blocks import TUNINGS, Block, activation_bytes, saves_input, unit_model
+from test_gpu_parity import check_norm_bwd, dec, st
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
+SHAPES = {"vit": dict(c=256, hidden=1024, heads=4), "llama": dict(c=256, hidden=688, heads=4)}
 
 
-def rel(a, b):
-    return float((a.float() - b.float()).norm() / b.float().norm())
+def make(arch, tuning, dtype=torch.bfloat16, norm_fp32=True, lora_init_b=0.0):
+    s = SHAPES[arch]
+    return Block(arch, s["c"], s["hidden"], s["heads"], tuning=tuning, dtype=dtype, device=DEV,
+                 norm_fp32=norm_fp32, lora_init_b=lora_init_b)
 
 
-@pytest.mark.parametrize("cls,c,h", [(ViTMLP, 768, 3072), (LlamaMLP, 512, 1376)])
-def test_forward_unchanged_and_ms_backward_exact(cls, c, h):
-    torch.manual_seed(0)
-    blk = cls(c, h, device=DEV)
-    x = synth.norm_input(256, c, "bf16").to(DEV)
-    ours_ms = blk.to_ours(act=False)          # merge + MS norm only: exact gradients
-    ours = blk.to_ours()                      # + ReGELU2 / ReSwiGLU2
-    xs = [x.clone().requires_grad_(True) for _ in range(3)]
-    outs = [m(xi) for m, xi in zip((blk, ours_ms, ours), xs)]
-    assert rel(outs[1], outs[0]) < 1e-2 and rel(outs[2], outs[0]) < 1e-2
-    dy = synth.grad_input(256, c, "bf16").to(DEV)
+def block_input(b, n, c, dtype=torch.bfloat16):
+    x = synth.norm_input(b * n, c, "bf16" if dtype == torch.bfloat16 else "f32").to(DEV)
+    return x.view(b, n, c).requires_grad_(True)
+
+
+@pytest.mark.parametrize("norm_fp32", [True, False])
+@pytest.mark.parametrize("tuning", TUNINGS)
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_saved_bytes_per_module(arch, tuning, norm_fp32):
+    b, n = 2, 96
+    exact = make(arch, tuning, norm_fp32=norm_fp32)
+    ours = exact.to_ours()
+    c, h = exact.c, exact.hidden
+    R = b * n
+    x = block_input(b, n, c)
+    te, pe = activation_bytes(exact, x, by_module=True)
+    to, po = activation_bytes(ours, x, by_module=True)
+    get = lambda d, k: d.get(k, 0)
+    # attention is untouched by the method
+    assert get(pe, "attn") == get(po, "attn") > 0
+    nb = 4 if norm_fp32 else 2                       # bytes / element of the reference norm's saved input
+    stats = 8 * R if arch == "vit" else 4 * R        # mean + rstd (LN) or rstd (RMS), fp32
+    for which, cons in ((1, ["q", "k", "v"]), (2, ["fc1"] if arch == "vit" else ["gate", "up"])):
+        name = f"norm{which}"
+        shared = exact.norm_shared(which)
+        assert get(pe, name) == nb * R * c + stats
+        assert get(po, name) == 2 * R * c + 4 * R                                # y + rstd
+        lora_small = sum(2 * R * exact.get_submodule(k).rank for k in cons if exact.modes[k] in ("lora", "lora_fa"))
+        # consumers: the exact block's consumers keep the norm output when condition 3 holds;
+        # ours keep nothing beyond it (y is the MS norm's, shared)
+        assert sum(get(pe, k) for k in cons) == (2 * R * c if shared else 0) + lora_small
+        assert sum(get(po, k) for k in cons) == lora_small
+        saving = get(pe, name) + sum(get(pe, k) for k in cons) - get(po, name) - sum(get(po, k) for k in cons)
+        if not shared and not norm_fp32:
+            assert saving == stats - 4 * R               # condition 3 fails: MS norm saves no tensor
+        elif not shared:
+            assert saving == 2 * R * c + stats - 4 * R   # only the fp32 -> 16-bit input, not the sharing
+        else:
+            assert saving == nb * R * c + stats - 4 * R  # the whole norm input: y is shared
+    # activation
+    if arch == "vit":
+        assert get(pe, "act") == 2 * R * h and get(po, "act") == P.codes_bytes(R * h)
+    else:
+        assert get(pe, "act") == 6 * R * h                                    # gate, silu(gate), up
+        assert get(po, "act") == 4 * R * h + P.codes_bytes(R * h)             # up, a, codes
+    assert te - to == sum(get(pe, k) - get(po, k) for k in set(pe) | set(po))
+
+
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_full_tuning_units_match_the_decoded_model(arch):
+    """Full tuning at the paper's expansion (ViT-B 4x, LLaMA-13B 2.7x): exact
+    vs ours in Fig. 5/6 units (unit = one [b, n, c] 16-bit tensor).  torch
+    SDPA returns its output in [b, n, h, d] layout, so the out-projection's
+    saved input IS the attention output (one unit less than the model's
+    separate kernels); attention statistics and norm rows add < 0.1 unit."""
+    c, h, heads = (768, 3072, 12) if arch == "vit" else (640, 1728, 5)   # 1728 / 640 = 2.7
+    blk = Block(arch, c, h, heads, tuning="full", device=DEV)
+    x = block_input(4, 128, c)
+    unit = 4 * 128 * c * 2
+    exact, ours = activation_bytes(blk, x) / unit, activation_bytes(blk.to_ours(), x) / unit
+    model = unit_model(arch, h / c)
+    assert abs(exact - (model["exact_units"] - 1)) < 0.1, (exact, model)
+    assert abs(ours - (model["ours_units"] - 1)) < 0.1, (ours, model)
+    assert 1 - ours / exact > model["saved_fraction"] - 0.01
+
+
+def _capture(block):
+    """Forward hooks recording the MS norms' input / output, the activation's
+    input and every uint8 / fp32-row tensor saved for backward."""
+    rec = {"saved": []}
+    hs = []
+    for name in ("norm1", "norm2", "act"):
+        m = block.get_submodule(name)
+        hs.append(m.register_forward_hook(lambda mod, a, o, n=name: rec.__setitem__(n, (a, o))))
+    for name in ("norm1", "norm2"):
+        m = block.get_submodule(name)
+        hs.append(m.register_full_backward_hook(lambda mod, gi, go, n=name: rec.__setitem__(n + "_bwd", (gi, go))))
+
+    def pack(t):
+        rec["saved"].append(t)
+        return t
+    return rec, hs, pack
+
+
+@pytest.mark.parametrize("tuning", ["full", "lora_qv", "lora_fa_all"])
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_block_internals_elementwise(arch, tuning):
+    blk = make(arch, tuning, lora_init_b=0.02).to_ours()
+    x = block_input(2, 64, blk.c)
+    rec, hs, pack = _capture(blk)
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = blk(x)
+    dy = synth.grad_input(x.numel() // blk.c, blk.c, "bf16").to(DEV).view_as(out)
+    out.backward(dy)
+    torch.cuda.synchronize()
+    for h in hs:
+        h.remove()
+    nf = P.msln_fwd if arch == "vit" else P.msrms_fwd
+    norm = "ln" if arch == "vit" else "rms"
+    for name in ("norm1", "norm2"):
+        (xin,), y = rec[name]
+        y_ref, r_ref = nf(xin.detach().contiguous(), blk.eps)
+        assert st(y).tobytes() == st(y_ref).tobytes(), name                  # bytewise, same input
+        rows = [t for t in rec["saved"] if t.dtype == torch.float32 and t.numel() == y_ref.numel() // blk.c]
+        assert any(torch.equal(t.reshape(-1), r_ref.reshape(-1)) for t in rows), f"{name}: rstd not saved"
+        # backward inside the block vs the oracle's Alg. 2 / Alg. 3 on the delivered gradient
+        (gin,), (gout,) = rec[name + "_bwd"]
+        Hc = blk.c
+        g2 = gout.detach().reshape(-1, Hc).cpu()
+        y64 = dec(y.detach().reshape(-1, Hc).cpu(), "bf16")
+        check_norm_bwd(norm, "bf16", g2, y64, r_ref.reshape(-1).cpu().numpy().astype(np.float64),
+                       gin.detach().reshape(-1, Hc))
+    # codes of the activation vs the oracle, bytewise
+    acts, _ = rec["act"]
+    pre = acts[0].detach().reshape(-1).cpu()
+    codes = [t for t in rec["saved"] if t.dtype == torch.uint8]
+    assert len(codes) == 1
+    _, c_ref = oracle.act_fwd("gelu" if arch == "vit" else "silu", dec(pre, "bf16"))
+    assert np.array_equal(codes[0].cpu().numpy(), c_ref)
+
+
+@pytest.mark.parametrize("tuning", ["full", "lora_all"])
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_merged_ms_block_gradient_equals_exact(arch, tuning):
+    """Affine merge + MS norms with the exact activation is exact BP
+    (S:L268): in fp32 the block input gradient matches the exact
+    block's elementwise, |d| <= 1e-4 (|g_i| + rms(g)) (fp32 reassociation
+    through the merged weights and the two backward formulas)."""
+    exact = make(arch, tuning, dtype=torch.float32, lora_init_b=0.05)
+    ours = exact.to_ours(act=False)
+    xs = [block_input(2, 64, exact.c, torch.float32) for _ in range(2)]
+    outs = [m(xi) for m, xi in zip((exact, ours), xs)]
+    assert torch.allclose(outs[0], outs[1], rtol=1e-4, atol=1e-4)
+    dy = synth.grad_input(128, exact.c, "f32").to(DEV).view_as(outs[0])
     for o in outs:
         o.backward(dy)
-    assert rel(xs[1].grad, xs[0].grad) < 2e-2                 # MS backward == exact backward
-    assert 0 < rel(xs[2].grad, xs[0].grad) < 0.6              # Approx-BP: close, not equal
+    g0, g1 = xs[0].grad.double(), xs[1].grad.double()
+    bound = 1e-4 * (g0.abs() + g0.pow(2).mean().sqrt())
+    assert bool(((g1 - g0).abs() <= bound).all()), float(((g1 - g0).abs() / bound).max())
+    # and the LoRA / trainable weights see the same gradients through the merge map (dB unchanged)
+    for name in exact.modes:
+        le, lo = exact.get_submodule(name), ours.get_submodule(name)
+        if le.lora_B is not None:
+            assert torch.allclose(le.lora_B.grad, lo.lora_B.grad, rtol=1e-3, atol=1e-5)
 
 
-def test_vit_block_saved_bytes():
-    R, c, h = 64 * 197 // 8, 768, 3072
-    blk = ViTMLP(c, h, device=DEV)
-    x = synth.norm_input(R, c, "bf16").to(DEV).requires_grad_(True)
-    exact = activation_bytes(blk, x)
-    ours = activation_bytes(blk.to_ours(), x)
-    assert ours == R * c * 2 + 4 * R + P.codes_bytes(R * h) + R * h * 2      # y(shared) + rstd + codes + fc2 in
-    unit = R * c * 2
-    assert exact / unit >= 10.9 and ours / unit <= 5.51                       # 11 -> 5.5 units (App. B)
-
-
-def test_llama_block_saved_bytes():
-    R, c, h = 512, 4096, 11008
-    blk = LlamaMLP(c, h, device=DEV)
-    x = synth.norm_input(R, c, "bf16").to(DEV).requires_grad_(True)
-    exact = activation_bytes(blk, x)
-    ours = activation_bytes(blk.to_ours(), x)
-    assert ours == R * c * 2 + 4 * R + 3 * R * h * 2 + P.codes_bytes(R * h)  # y + rstd + up, a, h + codes
-    assert exact > ours + 2 * R * c                                          # fp32 norm input and SiLU input gone
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_approx_block_trains(arch):
+    """ReGELU2 / ReSwiGLU2 inside the block: forward unchanged,
+    gradients close to but not equal to exact BP (Approx-BP)."""
+    exact = make(arch, "lora_all", lora_init_b=0.02)
+    ours = exact.to_ours()
+    xs = [block_input(2, 64, exact.c) for _ in range(2)]
+    outs = [m(xi) for m, xi in zip((exact, ours), xs)]
+    rel = lambda a, b: float((a.float() - b.float()).norm() / b.float().norm())
+    assert rel(outs[1], outs[0]) < 1e-2
+    dy = synth.grad_input(128, exact.c, "bf16").to(DEV).view_as(outs[0])
+    for o in outs:
+        o.backward(dy)
+    assert 0 < rel(xs[1].grad, xs[0].grad) < 0.6
+    assert saves_input("lora") and not saves_input("lora_fa")
