@@ -446,13 +446,14 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
 def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     """the table-driven k-bit step activation on the
     config's activation tensor -- k = 2 with the paper's table (bitwise equal
-    to the specialised kernel) and k = 4 -- GB/s of fwd + bwd."""
+    to the specialised kernel), k = 3 and k = 4 -- GB/s of fwd + bwd."""
     from paper_2406_16282_b200 import tables
     tab = tables.REGELU2 if cfg["act"] == "gelu" else tables.RESILU2
     b, n = x.element_size(), x.numel()
     y, dx = torch.empty_like(x), torch.empty_like(dy)
     out = {}
     for k, thr, lv in ((2, tab["c"], tables.levels(tab)),
+                       (3, [-3.0 + 1.0 * i for i in range(7)], [i / 7 for i in range(8)]),
                        (4, [-3.0 + 0.4 * i for i in range(15)], [i / 15 for i in range(16)])):
         codes = torch.empty(P.codes_bytes_k(n, k), dtype=torch.uint8, device=x.device)
         fns = (lambda: P.stepact_fwd(x, tab["act"], k, thr, y=y, codes=codes, stream=stream),
