@@ -17,12 +17,23 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "liblmbp.so")
 SOURCES = ["abi.cu", "act.cu", "norm.cu", "swiglu.cu", "stepact.cu", "fit.cu"]
-HEADERS = ["common.cuh", "constants.cuh", "kernels.h", "act_math.cuh", "ew_pipeline.cuh", os.path.join("..", "..", "include", "lmbp.h")]
+HEADERS = ["common.cuh", "constants.cuh", "kernels.h", "act_math.cuh", "act_lut.cuh", "ew_pipeline.cuh",
+           os.path.join("..", "..", "include", "lmbp.h"), os.path.join("..", "_obj", "act_lut.inc")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]
+         "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{os.path.join(HERE, '_obj')}"]
+LUT_INC = os.path.join(HERE, "_obj", "act_lut.inc")
+
+
+def ensure_lut() -> None:
+    """Generate the 16-bit forward tables (lut.py) into _obj/act_lut.inc when
+    missing or older than lut.py (build-time constants; not committed)."""
+    gen = os.path.join(HERE, "lut.py")
+    if _stale(LUT_INC, [gen]):
+        os.makedirs(os.path.dirname(LUT_INC), exist_ok=True)
+        subprocess.check_call([sys.executable, gen, LUT_INC])
 
 
 def _stale(target: str, deps) -> bool:
@@ -60,6 +71,7 @@ def build(force: bool = False) -> str:
     if force:
         for f in os.listdir(OBJ):
             os.remove(os.path.join(OBJ, f))
+    ensure_lut()
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(_compile, SOURCES))
     if force or _stale(LIB, objs):
@@ -70,7 +82,7 @@ def build(force: bool = False) -> str:
     return LIB
 
 
-def build_variant(name: str, defines) -> str:
+def build_variant(name: str, defines, sources=None) -> str:
     """Tuning aid: build liblmbp_<name>.so with extra -D defines into
     _variants/ (used by tools/sweep.py; the product library is LIB)."""
     import hashlib
@@ -78,8 +90,12 @@ def build_variant(name: str, defines) -> str:
     name = f"{name}-{tag}"                     # same name, different -D set: a different build
     vdir = os.path.join(HERE, "_variants", name)
     os.makedirs(vdir, exist_ok=True)
-    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, vdir, defines), SOURCES))
+    ensure_lut()
+    srcs = SOURCES if sources is None else list(sources)
+    with cf.ThreadPoolExecutor(len(srcs)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, vdir, defines), srcs))
+    # sources left out are linked from the product build (knob-independent, e.g. fit.cu)
+    objs += [_compile(s) for s in SOURCES if s not in srcs]
     out = os.path.join(HERE, "_variants", f"liblmbp_{name}.so")
     if _stale(out, objs) or not os.path.exists(out):
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])

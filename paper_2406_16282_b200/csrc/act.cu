@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "act_math.cuh"
+#include "act_lut.cuh"
 #include "ew_pipeline.cuh"
 #include "kernels.h"
 
@@ -35,7 +36,7 @@ __device__ void act_fwd_tail(const T *x, T *y, uint8_t *codes, int64_t j0, int64
       const int64_t j = 4 * b + k;
       if (j >= n) break;
       const float f = to_f32<T>(x[j]);
-      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+      y[j] = act_y<T, A, kPrecise>(x[j], f);
       byte |= code_f32<A>(f) << (2 * k);
     }
     codes[b] = (uint8_t)byte;
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) act_fwd_scalar(const T *x, T *y, uint8_t 
       const int64_t j = 4 * b + k;
       if (j < n) {
         const float f = to_f32<T>(x[j]);
-        y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+        y[j] = act_y<T, A, kPrecise>(x[j], f);
         byte |= code_f32<A>(f) << (2 * k);
       }
     }
@@ -193,6 +194,46 @@ struct ActFwdOp {
   }
 };
 
+// GELU on 16-bit types (kUseLut): the correctly rounded table (act_lut.cuh)
+// copied to shared memory once per CTA; one LDS per element instead of the
+// polynomial / MUFU math; codes as before (packed compares).  Tail elements
+// read the same table.
+#ifndef LMBP_LUT_W
+#define LMBP_LUT_W 16
+#define LMBP_LUT_U 2
+#define LMBP_LUT_S 4
+#endif
+template <typename T, int A>
+struct ActFwdLutOp {
+  static_assert(sizeof(T) == 2, "16-bit types only");
+  static constexpr bool kTab16 = true;
+  static constexpr int W = LMBP_LUT_W, U = LMBP_LUT_U, S = LMBP_LUT_S, kIn = 1, kCodeIn = 0, kCodeOut = 2;
+  __device__ static const uint16_t *tab16() { return lut16<T, A>(); }
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p, uint32_t tab) {
+    const uint32_t c = codes_vec_16<T, A>(v[0]);
+    st_stream(p.out[0] + i, make_uint4(tab16_pair(tab, v[0].x), tab16_pair(tab, v[0].y), tab16_pair(tab, v[0].z),
+                                       tab16_pair(tab, v[0].w)));
+    return c;
+  }
+  __device__ static void tail(const EwParams &p, uint32_t tab) {
+    const int64_t j0 = p.nvec * 8;
+    if (j0 >= p.n) return;
+    const T *x = reinterpret_cast<const T *>(p.in[0]);
+    uint16_t *y = reinterpret_cast<uint16_t *>(p.out[0]);
+    for (int64_t b = j0 >> 2; 4 * b < p.n; ++b) {
+      uint32_t byte = 0;
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = 4 * b + k;
+        if (j >= p.n) break;
+        const uint16_t xb = reinterpret_cast<const uint16_t *>(x)[j];
+        y[j] = (uint16_t)lds_u16(tab + 2u * xb);
+        byte |= code_f32<A>(to_f32<T>(x[j])) << (2 * k);
+      }
+      p.codes_out[b] = (uint8_t)byte;
+    }
+  }
+};
+
 template <typename T, int A>
 __device__ void act_bwd_tail(const T *dy, const uint8_t *codes, T *dx, int64_t j0, int64_t n) {
   for (int64_t j = j0; j < n; ++j) {
@@ -201,9 +242,18 @@ __device__ void act_bwd_tail(const T *dy, const uint8_t *codes, T *dx, int64_t j
   }
 }
 
+// Backward shape: 12 consumer warps x 4 vectors (24 KB tiles + codes) x 2
+// stages (was 3: C2 26.6 -> 24.6 us, C4/C5 unchanged -- a shallower ring
+// leaves less queued work per CTA to drain at the end, profiles/r02/sweep38).
+#ifndef LMBP_BWD_W
+#define LMBP_BWD_W 12
+#define LMBP_BWD_U 4
+#define LMBP_BWD_S 2
+#endif
 template <typename T, int A>
 struct ActBwdOp {
-  static constexpr int W = 12, U = 4, S = 3, kIn = 1, kCodeIn = Traits<T>::kVec / 4, kCodeOut = 0;
+  static constexpr int W = LMBP_BWD_W, U = LMBP_BWD_U, S = LMBP_BWD_S, kIn = 1, kCodeIn = Traits<T>::kVec / 4,
+                       kCodeOut = 0;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t c, int64_t i, const EwParams &p) {
     return act_vec_op<T, A, false, false>(v[0], c, p.out[0], i);
   }
@@ -243,7 +293,11 @@ static cudaError_t act_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, 
     p.codes_out = codes;
     p.nvec = n / kVec;
     p.n = n;
-    return launch_ew<ActFwdOp<T, A, kPrecise>>(p, s);
+#ifndef LMBP_NO_LUT
+    if constexpr (kUseLut<T, A>) return launch_ew<ActFwdLutOp<T, A>>(p, s);
+    else
+#endif
+      return launch_ew<ActFwdOp<T, A, kPrecise>>(p, s);
   } else {
     auto kern = act_fwd_scalar<T, A, kPrecise>;
     static const int occ = occupancy(kern, kActThreads);
@@ -309,3 +363,20 @@ cudaError_t act_bwd(int kind, int dtype, const void *dy, const uint8_t *codes, v
 }
 
 }  // namespace lmbp
+
+#ifdef LMBP_TRACE
+// Diagnostic build only: read / reset this translation unit's CTA trace.
+extern "C" __attribute__((visibility("default"))) int lmbp_trace_act(unsigned long long *host, int max_records,
+                                                                    int reset) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, lmbp::lmbp_trace_n, sizeof(n)) != cudaSuccess) return -1;
+  const int m = (int)(n < (unsigned)max_records ? n : (unsigned)max_records);
+  if (m > 0 && cudaMemcpyFromSymbol(host, lmbp::lmbp_trace_buf, (size_t)m * 5 * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  if (reset) {
+    const unsigned int z = 0;
+    if (cudaMemcpyToSymbol(lmbp::lmbp_trace_n, &z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return m;
+}
+#endif

@@ -49,17 +49,34 @@ template <class Op> struct MinBlocksOf<Op, std::void_t<decltype(Op::kMinBlocks)>
   static constexpr int value = Op::kMinBlocks;
 };
 
+// Optional 16-bit lookup table (the ReGELU2 / ReSiLU2 forward of 16-bit
+// types, lut.py): an Op with `static constexpr bool kTab16 = true` and
+// `__device__ static const uint16_t *tab16()` (a 65536-entry table in global
+// memory) gets it copied once per CTA into the first 128 KB of shared memory
+// (bulk copies on their own mbarrier, issued by the producer before the first
+// tile) and receives its shared-window address as a trailing `uint32_t`
+// argument of apply().
+template <class Op, class = void> struct Tab16Of { static constexpr bool value = false; };
+template <class Op> struct Tab16Of<Op, std::void_t<decltype(Op::kTab16)>> { static constexpr bool value = Op::kTab16; };
+constexpr uint32_t kTab16Bytes = 65536 * 2;
+
 template <class Op> struct EwShape {
+  static constexpr size_t kTabBytes = Tab16Of<Op>::value ? kTab16Bytes : 0;
   static constexpr int kTile = Op::W * 32 * Op::U;  // vectors per tile
   static constexpr int kThreads = (Op::W + 1) * 32;
   static constexpr size_t kStageBytes = (size_t)Op::kIn * kTile * 16 + (size_t)Op::kCodeIn * kTile;
   // per-warp staging of the codes a warp writes for one tile (32 U words)
   static constexpr size_t kWarpCodeBytes = (size_t)32 * Op::U * Op::kCodeOut;
   static constexpr size_t kCodeStage = (size_t)Op::W * kWarpCodeBytes;
-  // stages | code staging | full[S] empty[S] clc_bar (+pad) | slot[S+1] | clc response (16 B)
+  // [table] | stages | code staging | full[S] empty[S] clc_bar tab_bar | slot[S+1] | clc response (16 B)
   static constexpr size_t kBarBytes = (2 * (size_t)Op::S + 2) * sizeof(uint64_t);
   static constexpr size_t kSlotBytes = (((size_t)Op::S + 1) * sizeof(int64_t) + 15) / 16 * 16;
-  static constexpr size_t kSmem = (size_t)Op::S * kStageBytes + kCodeStage + kBarBytes + kSlotBytes + 16;
+  static constexpr size_t kSmemUsed = kTabBytes + (size_t)Op::S * kStageBytes + kCodeStage + kBarBytes + kSlotBytes + 16;
+#ifdef LMBP_EW_ONE_CTA  // tuning knob: request > half the SM's shared memory so one CTA runs per SM
+  static constexpr size_t kSmem = kSmemUsed > 116 * 1024 ? kSmemUsed : 116 * 1024;
+#else
+  static constexpr size_t kSmem = kSmemUsed;
+#endif
   static_assert(kStageBytes % 16 == 0, "stage must stay 16-byte aligned");
   static_assert(kWarpCodeBytes % 16 == 0, "code staging must stay 16-byte aligned");
 };
@@ -106,23 +123,60 @@ template <class Op> struct LutOf<Op, std::void_t<decltype(Op::kLut)>> { static c
 
 template <class Op, class P, int NIN>
 __device__ __forceinline__ uint32_t apply_op(const uint4 (&v)[NIN], uint32_t c, int64_t i, const P &p,
-                                             const float *lut) {
+                                             const float *lut, uint32_t tab) {
   if constexpr (LutOf<Op>::value > 0) return Op::apply(v, c, i, p, lut);
+  else if constexpr (Tab16Of<Op>::value) return Op::apply(v, c, i, p, tab);
   else return Op::apply(v, c, i, p);
+}
+
+#ifdef LMBP_TRACE
+// Diagnostic build only (tools/trace_ew.py): one record per running CTA --
+// smid, entry time, first tile's data arrival, last tile done, tiles -- in
+// globaltimer nanoseconds.  Each translation unit has its own buffer.
+static __device__ unsigned long long lmbp_trace_buf[8192 * 5];
+static __device__ unsigned int lmbp_trace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+// One 16-bit table entry from shared memory (tab = shared-window address).
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(r) : "r"(addr));
+  return r;
+}
+// Two packed 16-bit inputs -> two packed 16-bit table outputs.
+// The halves are extracted with PRMT so each address is PRMT + LEA (2 issue
+// slots; written as shifts and masks ptxas emits IADD + LOP3 + IADD).
+__device__ __forceinline__ uint32_t tab16_pair(uint32_t tab, uint32_t w) {
+  const uint32_t lo = lds_u16(tab + 2u * __byte_perm(w, 0u, 0x4410));
+  const uint32_t hi = lds_u16(tab + 2u * __byte_perm(w, 0u, 0x4432));
+  return __byte_perm(lo, hi, 0x5410);
 }
 
 template <class Op>
 __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value) ew_tma(const typename ParamsOf<Op>::type p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_all[];
   using Sh = EwShape<Op>;
   constexpr int W = Op::W, U = Op::U, S = Op::S, NIN = Op::kIn, TILE = Sh::kTile;
+  const uint32_t tab = smem_u32(smem_all);                  // the 16-bit table (when Tab16Of<Op>)
+  uint8_t *smem = smem_all + Sh::kTabBytes;                 // stages
   uint8_t *cstage = smem + (size_t)S * Sh::kStageBytes;  // codes staging, one slice per warp
   uint64_t *full = reinterpret_cast<uint64_t *>(cstage + Sh::kCodeStage);
   uint64_t *empty = full + S;
   uint64_t *clc_bar = empty + S;
+  uint64_t *tab_bar = clc_bar + 1;
   int64_t *slot = reinterpret_cast<int64_t *>(clc_bar + 2);   // tile index held by each stage
   uint4 *clc_resp = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(slot) + Sh::kSlotBytes);  // 16 B aligned
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LMBP_TRACE
+  const unsigned long long tr_entry = gtimer();
+  unsigned long long tr_first = 0;
+  unsigned int tr_tiles = 0;
+#endif
   const int64_t ntiles = p.nvec / TILE;
   const int64_t nitems = ntiles + 1;                           // + the leftover pseudo-tile
 
@@ -139,12 +193,20 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
       mbar_init(&empty[s], W);
     }
     mbar_init(clc_bar, 1);
+    mbar_init(tab_bar, 1);
     mbar_fence_init();
   }
   __syncthreads();
 
   if (warp == W) {  // producer
     if (lane == 0) {
+      if constexpr (Tab16Of<Op>::value) {
+        mbar_arrive_expect_tx(tab_bar, kTab16Bytes);
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(Op::tab16());
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          bulk_g2s(smem_all + q * (kTab16Bytes / 4), src + q * (kTab16Bytes / 4), kTab16Bytes / 4, tab_bar);
+      }
       int k = 0;
       int64_t unit = blockIdx.x;
       uint32_t clc_phase = 0;
@@ -184,10 +246,15 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
     return;
   }
 
+  if constexpr (Tab16Of<Op>::value) mbar_wait(tab_bar, 0);
   for (int k = 0;; ++k) {
     const int s = k % S;
     mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
     const int64_t t = slot[s];
+#ifdef LMBP_TRACE
+    if (k == 0) tr_first = gtimer();
+    ++tr_tiles;
+#endif
     if (t < 0) break;
     if (t == ntiles) {
       // Leftover vectors (< one tile) with direct loads, then the ragged tail.
@@ -197,10 +264,13 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         uint4 v[NIN];
 #pragma unroll
         for (int m = 0; m < NIN; ++m) v[m] = ld_stream(p.in[m] + i);
-        const uint32_t co = apply_op<Op>(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p, lut);
+        const uint32_t co = apply_op<Op>(v, code_word<Op::kCodeIn>(p.codes_in, i), i, p, lut, tab);
         put_code<Op::kCodeOut>(p.codes_out, i, co);
       }
-      if (threadIdx.x == 0) Op::tail(p);
+      if (threadIdx.x == 0) {
+        if constexpr (Tab16Of<Op>::value) Op::tail(p, tab);
+        else Op::tail(p);
+      }
       continue;
     }
     const uint8_t *st = smem + (size_t)s * Sh::kStageBytes;
@@ -220,7 +290,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
     const int64_t wbase = t * TILE + warp * (32 * U);
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const uint32_t co = apply_op<Op>(v[j], c[j], wbase + j * 32 + lane, p, lut);
+      const uint32_t co = apply_op<Op>(v[j], c[j], wbase + j * 32 + lane, p, lut, tab);
       if constexpr (Op::kCodeOut > 0) put_code<Op::kCodeOut>(cstage + warp * Sh::kWarpCodeBytes, j * 32 + lane, co);
     }
     if constexpr (Op::kCodeOut > 0) {
@@ -236,6 +306,21 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
       __syncwarp();
     }
   }
+#ifdef LMBP_TRACE
+  if (threadIdx.x == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const unsigned int r = atomicAdd(&lmbp_trace_n, 1u);
+    if (r < 8192) {
+      unsigned long long *b = lmbp_trace_buf + 5 * r;
+      b[0] = smid;
+      b[1] = tr_entry;
+      b[2] = tr_first;
+      b[3] = gtimer();
+      b[4] = tr_tiles - 1;
+    }
+  }
+#endif
 }
 
 // Launch one CTA per work unit; resident CTAs steal the rest through CLC.

@@ -14,6 +14,7 @@
 // 8 fill exactly k whole bytes, so a thread (or a 16-byte vector of 8 16-bit
 // elements) owns k bytes of codes; for k = 3 a single code may straddle two
 // of those bytes (handled by building the group's 24-bit word first).
+#include "act_lut.cuh"
 #include "act_math.cuh"
 #include "common.cuh"
 #include "ew_pipeline.cuh"
@@ -99,11 +100,15 @@ __global__ void __launch_bounds__(256) stepact_fwd_k(const T *x, T *y, uint8_t *
     load8<T>(x, g, vec, f);
     uint32_t w = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      w |= step_code<K>(f[e], tab.thr) << (K * e);
-      f[e] = act_f<A, kPrecise>(f[e]);
+    for (int e = 0; e < 8; ++e) w |= step_code<K>(f[e], tab.thr) << (K * e);
+    if constexpr (kUseLut<T, A>) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[8 * g + e] = act_y<T, A, kPrecise>(from_f32<T>(f[e]), f[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = act_f<A, kPrecise>(f[e]);
+      store8<T>(y, g, vec, f);
     }
-    store8<T>(y, g, vec, f);
 #pragma unroll
     for (int b = 0; b < K; ++b) codes[g * K + b] = (uint8_t)(w >> (8 * b));
   }
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(256) stepact_fwd_k(const T *x, T *y, uint8_t *
     for (int64_t j = groups * 8; j < n; ++j) {
       const float f = to_f32<T>(x[j]);
       w |= step_code<K>(f, tab.thr) << (K * (j - groups * 8));
-      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+      y[j] = act_y<T, A, kPrecise>(x[j], f);
     }
     const int nbytes = (int)(((n - groups * 8) * K + 7) / 8);
     for (int b = 0; b < nbytes; ++b) codes[groups * K + b] = (uint8_t)(w >> (8 * b));
@@ -239,10 +244,22 @@ struct StepFwdOp {
   // (it would spill at 48) and fp32: 16 x 4, 2 CTAs / SM (profiles/r01/sweep32_*, sweep33_*: C4 96.4 -> 94.3 us,
   // C5 443 -> 429 us; the 16-bit shape costs C3 fp32 +2 %, so fp32 keeps its own).
   static constexpr bool k16 = sizeof(T) == 2 && A == kActSilu;  // GELU's math needs > 48 registers
-  static constexpr int kMinBlocks = K == 4 ? (k16 ? LMBP_STEP_MINB4 : LMBP_STEP_MINB4_F32) : 0;
+#ifndef LMBP_NO_LUT
+  // y from the correctly rounded table where regelu2_fwd / resilu2_fwd take
+  // it (kUseLut: GELU on 16-bit types), so k = 2 with the paper's table stays
+  // bitwise equal to them; 128 KB of shared memory -> one CTA per SM.
+  static constexpr bool kTab16 = kUseLut<T, A>;
+#else
+  static constexpr bool kTab16 = false;
+#endif
+  __device__ static const uint16_t *tab16() {
+    if constexpr (kUseLut<T, A>) return lut16<T, A>();
+    else return nullptr;
+  }
+  static constexpr int kMinBlocks = kTab16 ? 0 : K == 4 ? (k16 ? LMBP_STEP_MINB4 : LMBP_STEP_MINB4_F32) : 0;
   static constexpr int kVecT = Traits<T>::kVec;
-  static constexpr int W = K == 4 && k16 ? LMBP_STEP4_W : LMBP_STEP_W, U = LMBP_STEP_U,
-                       S = K == 4 && k16 ? LMBP_STEP4_S : LMBP_STEP_S, kIn = 1, kCodeIn = 0,
+  static constexpr int W = kTab16 ? LMBP_STEP_W : K == 4 && k16 ? LMBP_STEP4_W : LMBP_STEP_W, U = LMBP_STEP_U,
+                       S = kTab16 ? LMBP_STEP_S : K == 4 && k16 ? LMBP_STEP4_S : LMBP_STEP_S, kIn = 1, kCodeIn = 0,
                        kCodeOut = kVecT * K / 8;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p) {
     float f[kVecT];
@@ -257,7 +274,14 @@ struct StepFwdOp {
     st_stream(p.out[0] + i, Vec<T>::pack(f));
     return w;
   }
-  __device__ static void tail(const StepEwParams &p) {
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p, uint32_t tab) {
+    float f[kVecT];  // unused by the 16-bit code search
+    const uint32_t w = step_codes_vec<T, K>(v[0], f, p.tab);
+    st_stream(p.out[0] + i, make_uint4(tab16_pair(tab, v[0].x), tab16_pair(tab, v[0].y), tab16_pair(tab, v[0].z),
+                                       tab16_pair(tab, v[0].w)));
+    return w;
+  }
+  __device__ static void tail(const StepEwParams &p, uint32_t tab = 0) {
     const int64_t j0 = p.nvec * kVecT;
     if (j0 >= p.n) return;
     const T *x = reinterpret_cast<const T *>(p.in[0]);
@@ -266,7 +290,12 @@ struct StepFwdOp {
     for (int64_t j = j0; j < p.n; ++j) {
       const float f = to_f32<T>(x[j]);
       w |= step_code<K>(f, p.tab.thr) << (K * (j - j0));
-      y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+      if constexpr (kTab16) {
+        const uint16_t b = (uint16_t)lds_u16(tab + 2u * reinterpret_cast<const uint16_t *>(x)[j]);
+        y[j] = *reinterpret_cast<const T *>(&b);
+      } else {
+        y[j] = from_f32<T>(act_f<A, kPrecise>(f));
+      }
     }
     const int nbytes = (int)(((p.n - j0) * K + 7) / 8);
     for (int b = 0; b < nbytes; ++b) p.codes_out[j0 * K / 8 + b] = (uint8_t)(w >> (8 * b));

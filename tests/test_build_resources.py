@@ -29,10 +29,10 @@ def test_pipeline_register_budgets():
     r = regs("act.ptxas.log")
     d = demangle(list(r))
     by = {d[k]: v for k, v in r.items()}
-    fwd = [v for k, v in by.items() if "ActFwdOp<__nv_bfloat16" in k]
+    fwd = [v for k, v in by.items() if "ActFwdOp<__nv_bfloat16, 1" in k]
     bwd = [v for k, v in by.items() if "ActBwdOp<__nv_bfloat16" in k]
     assert fwd and bwd
-    # forward CTA = 17 warps (544 threads): 2 CTAs / SM need <= 60 registers
+    # SiLU 16-bit forward CTA = 17 warps (544 threads): 2 CTAs / SM need <= 60 registers
     assert max(fwd) <= 60, by
     # backward CTA = 13 warps (416 threads): 2 CTAs / SM need <= 78 registers
     assert max(bwd) <= 78, by
@@ -48,18 +48,33 @@ def test_no_spills_in_hot_kernels():
 
 @pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "stepact.ptxas.log")), reason="no build logs")
 def test_kbit_forward_register_budget():
-    """k = 4 SiLU forward, 16-bit types: 13-warp CTAs (416 threads), 3 per SM
-    need <= 52 registers (ptxas targets 48); no step forward spills (sweep33)."""
+    """16-bit step forwards read y from the 128 KB table (one CTA of 17 warps
+    per SM: <= 120 registers); fp32 k = 4 keeps 2 CTAs / SM (<= 60); no step
+    forward spills."""
     r = regs("stepact.ptxas.log")
     d = demangle(list(r))
     by = {d[k]: v for k, v in r.items()}
-    k4 = [v for k, v in by.items() if re.search(r"StepFwdOp<(__nv_bfloat16|__half), 1, false, 4>", k)]
-    assert len(k4) == 2, by
-    assert max(k4) <= 52, by
+    k16 = [v for k, v in by.items() if re.search(r"StepFwdOp<(__nv_bfloat16|__half), 0, false, [1234]>", k)]
+    silu4 = [v for k, v in by.items() if re.search(r"StepFwdOp<(__nv_bfloat16|__half), 1, false, 4>", k)]
+    k32 = [v for k, v in by.items() if re.search(r"StepFwdOp<float, [01], true, 4>", k)]
+    assert len(k16) == 8 and len(silu4) == 2 and len(k32) == 2, by
+    # GELU 16-bit reads the table (1 CTA / SM: <= 120); SiLU k = 4 keeps 3 x 416-thread CTAs (<= 52)
+    assert max(k16) <= 120 and max(silu4) <= 52 and max(k32) <= 60, by
     text = open(os.path.join(OBJ, "stepact.ptxas.log")).read()
     for m in re.finditer(r"Function properties for (\S+)\n.*?(\d+) bytes spill stores", text):
         if "StepFwdOp" in demangle([m.group(1)])[m.group(1)]:
             assert int(m.group(2)) == 0, m.group(1)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "act.ptxas.log")), reason="no build logs")
+def test_lut_forward_fits_one_cta_per_sm():
+    """The 16-bit forward (ActFwdLutOp): 544-thread CTAs, one per SM next to
+    its 128 KB table, so <= 120 registers."""
+    r = regs("act.ptxas.log")
+    d = demangle(list(r))
+    lut = [v for k, v in d.items() if "ActFwdLutOp" in v]
+    assert len(lut) == 2                          # GELU bf16 / fp16 (kUseLut)
+    assert max(r[k] for k, v in d.items() if "ActFwdLutOp" in v) <= 120
 
 
 @pytest.mark.skipif(not os.path.exists(os.path.join(OBJ, "norm.ptxas.log")), reason="no build logs")

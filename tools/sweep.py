@@ -26,8 +26,9 @@ DT = {"f32": 0, "bf16": 1, "f16": 2}
 def load(path):
     L = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
-        f = getattr(L, name)
-        f.restype, f.argtypes = res, args
+        f = getattr(L, name, None)          # sweep variants are built without the fitter
+        if f is not None:
+            f.restype, f.argtypes = res, args
     return L
 
 
@@ -38,6 +39,8 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--kernels", default="act_fwd,act_bwd,norm_fwd,norm_bwd")
     ap.add_argument("--build-only", action="store_true")
+    ap.add_argument("--sources", default=None, help="comma list of .cu files compiled with the variant's -D set "
+                                                     "(the rest are linked from the product build)")
     ap.add_argument("--yoff", type=int, default=0, help="offset y by this many bytes (address-interaction probe)")
     a = ap.parse_args()
     libs = {}
@@ -46,7 +49,9 @@ def main():
         if defs.startswith("@"):          # a prebuilt library, e.g. from another commit
             libs[name] = os.path.join(ROOT, defs[1:])
         else:
-            libs[name] = B.build_variant(name, [d for d in defs.split(",") if d])
+            libs[name] = B.build_variant(name, [d for d in defs.split(",") if d],
+                                         sources=(a.sources.split(",") if a.sources else
+                                                  [s for s in B.SOURCES if s != "fit.cu"]))
     if a.build_only:
         return
     cfg = synth.CONFIGS[a.config]
@@ -102,6 +107,11 @@ def main():
         calls["norm_fwd"]()
         calls["step4_fwd"]()
         for k in a.kernels.split(","):
+            rc0 = calls[k]()
+            if rc0 != 0:                      # e.g. a shape the GPU refuses (> 1024 threads)
+                torch.cuda.synchronize()
+                print(json.dumps({"variant": name, "config": a.config, "kernel": k, "error": rc0}), flush=True)
+                continue
             for _ in range(3):
                 calls[k]()
             ts = []
