@@ -586,7 +586,10 @@ static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   // 16 bits) take the per-warp ring instead.
   if (V > 4) return p;
   const size_t stage = (size_t)nvec * 16 * (fwd ? 1 : 2);
-  int stages = (int)std::min<size_t>(4, (size_t)(LMBP_ROW_STAGE_KB * 1024) / stage);
+#ifndef LMBP_ROW_MAXST
+#define LMBP_ROW_MAXST 4
+#endif
+  int stages = (int)std::min<size_t>(LMBP_ROW_MAXST, (size_t)(LMBP_ROW_STAGE_KB * 1024) / stage);
   if (stages < 2) stages = 2;
   const size_t tail = 16 + (2 * (size_t)stages + 1) * 8 + (size_t)stages * 8 + 64 * sizeof(float2) +
                       (size_t)stages * sizeof(float);

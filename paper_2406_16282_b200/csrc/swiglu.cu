@@ -17,6 +17,18 @@
 #include "ew_pipeline.cuh"
 #include "kernels.h"
 
+// Pipeline shapes (tools/sweep.py knobs): consumer warps x vectors per lane x stages.
+#ifndef LMBP_SWF_W
+#define LMBP_SWF_W 16
+#define LMBP_SWF_U 2
+#define LMBP_SWF_S 3
+#endif
+#ifndef LMBP_SWB_W
+#define LMBP_SWB_W 12
+#define LMBP_SWB_U 2
+#define LMBP_SWB_S 3
+#endif
+
 namespace lmbp {
 
 template <typename T, bool kPrecise>
@@ -35,7 +47,8 @@ __device__ __forceinline__ void swiglu_bwd_elem(float dh, float u, float a, uint
 
 template <typename T, bool kPrecise>
 struct SwiGluFwdOp {
-  static constexpr int W = 16, U = 2, S = 3, kIn = 2, kCodeIn = 0, kCodeOut = Traits<T>::kVec / 4;
+  static constexpr int W = LMBP_SWF_W, U = LMBP_SWF_U, S = LMBP_SWF_S, kIn = 2, kCodeIn = 0,
+                       kCodeOut = Traits<T>::kVec / 4;
   __device__ static uint32_t apply(const uint4 (&v)[2], uint32_t, int64_t i, const EwParams &p) {
     constexpr int kVec = Traits<T>::kVec;
     float g[kVec], u[kVec], a[kVec];
@@ -79,7 +92,8 @@ struct SwiGluFwdOp {
 
 template <typename T>
 struct SwiGluBwdOp {
-  static constexpr int W = 12, U = 2, S = 3, kIn = 3, kCodeIn = Traits<T>::kVec / 4, kCodeOut = 0;
+  static constexpr int W = LMBP_SWB_W, U = LMBP_SWB_U, S = LMBP_SWB_S, kIn = 3, kCodeIn = Traits<T>::kVec / 4,
+                       kCodeOut = 0;
   __device__ static uint32_t apply(const uint4 (&v)[3], uint32_t c, int64_t i, const EwParams &p) {
     constexpr int kVec = Traits<T>::kVec;
     float dh[kVec], u[kVec], a[kVec];

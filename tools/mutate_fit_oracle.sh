@@ -2,13 +2,14 @@
 # Mutation check for the fitter-oracle pins: apply one python-level text
 # substitution to oracle/fit.py, run tests/test_fit_oracle.py, restore.
 # Every mutation below must make at least one pin fail.
-cd "$(dirname "$0")/.."
-mkdir -p /tmp/mut
-# never start from (or leave behind) a mutant: the file must match git HEAD,
-# and it is restored on any exit (an interrupted run once left one behind)
-git diff --quiet HEAD -- oracle/fit.py || { echo "oracle/fit.py differs from HEAD; refusing"; exit 1; }
-cp oracle/fit.py /tmp/mut/fit_orig.py
-trap 'cp /tmp/mut/fit_orig.py oracle/fit.py' EXIT
+# Runs in a scratch copy of the repository: the committed oracle/fit.py is
+# never edited (a mutant once reached a commit when this edited in place).
+SRC="$(cd "$(dirname "$0")/.." && pwd)"
+SCR="$(mktemp -d /tmp/lmbp_fitmut.XXXXXX)"
+trap 'rm -rf "$SCR"' EXIT
+tar -C "$SRC" --exclude=.git --exclude=gpurun_out --exclude='*.so' --exclude=_obj --exclude=_variants -cf - . | tar -C "$SCR" -xf -
+cd "$SCR"
+cp oracle/fit.py /tmp/lmbp_fit_orig.py
 run() {
   python - "$1" "$2" <<'PY'
 import sys
@@ -19,7 +20,7 @@ open(p, "w").write(s.replace(old, new, 1))
 PY
   echo "== $1  ->  $2"
   timeout 900 python -m pytest tests/test_fit_oracle.py -q -x 2>&1 | tail -1
-  cp /tmp/mut/fit_orig.py oracle/fit.py
+  cp /tmp/lmbp_fit_orig.py oracle/fit.py
 }
 run 'math.sqrt(-2.0 * math.log(eps))' 'math.sqrt(-math.log(eps))'                       # GELU tail bound
 run '-2.0 * math.log(eps / 2.0)' '-2.0 * math.log(eps)'                                 # SiLU tail bound

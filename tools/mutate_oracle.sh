@@ -1,16 +1,16 @@
 #!/bin/bash
-# Mutation check for the oracle pins: apply one sed edit to oracle/oracle.c,
-# run tests/test_oracle_pins.py, restore.  Every mutation listed in DESIGN.md
-# ("Oracle pins") must make at least one pin fail.
-# usage: run.sh 'sed-expr'
-cd "$(dirname "$0")/.."
-mkdir -p /tmp/mut
-git diff --quiet HEAD -- oracle/oracle.c || { echo "oracle/oracle.c differs from HEAD; refusing"; exit 1; }
-cp oracle/oracle.c /tmp/mut/orig.c
-trap 'cp /tmp/mut/orig.c oracle/oracle.c; rm -f oracle/liboracle.so' EXIT
+# Mutation check for the oracle pins: copy the repository to a scratch
+# directory, apply one sed edit to the COPY's oracle/oracle.c, run the copy's
+# tests/test_oracle_pins.py.  The committed oracle is never touched.  Every
+# mutation listed in DESIGN.md ("Oracle pins") must make at least one pin fail.
+# usage: mutate_oracle.sh 'sed-expr'
+set -e
+SRC="$(cd "$(dirname "$0")/.." && pwd)"
+SCR="$(mktemp -d /tmp/lmbp_mut.XXXXXX)"
+trap 'rm -rf "$SCR"' EXIT
+tar -C "$SRC" --exclude=.git --exclude=gpurun_out --exclude='*.so' --exclude=_obj --exclude=_variants -cf - . | tar -C "$SCR" -xf -
+cd "$SCR"
+cp oracle/oracle.c /tmp/lmbp_mut_orig.c
 sed -i "$1" oracle/oracle.c
-if cmp -s oracle/oracle.c /tmp/mut/orig.c; then echo "NO CHANGE: $1"; fi
-rm -f oracle/liboracle.so
-timeout 600 python -m pytest tests/test_oracle_pins.py -q 2>&1 | tail -1
-cp /tmp/mut/orig.c oracle/oracle.c
-rm -f oracle/liboracle.so
+if cmp -s oracle/oracle.c /tmp/lmbp_mut_orig.c; then echo "NO CHANGE: $1"; fi
+timeout 600 python -m pytest tests/test_oracle_pins.py -q -p no:cacheprovider 2>&1 | tail -1

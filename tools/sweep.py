@@ -62,6 +62,7 @@ def main():
     ybuf = torch.empty(x.numel() * x.element_size() + a.yoff, dtype=torch.uint8, device=dev)
     y = ybuf[a.yoff:].view(x.dtype).view(x.shape)
     dx = torch.empty_like(dy)
+    x2, y2 = torch.empty_like(dy), torch.empty_like(dy)
     codes = torch.empty((R * F + 3) // 4, dtype=torch.uint8, device=dev)
     codes4 = torch.empty((R * F + 1) // 2, dtype=torch.uint8, device=dev)
     thr2 = (ctypes.c_double * 3)(-3.1858810036855245, -0.001178821281161997, 3.190832613414926)
@@ -81,7 +82,8 @@ def main():
     nbytes = {"ncopy": 2 * b * R * H, "copy": 2 * b * n, "act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
               "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R,
               "step2_fwd": 2 * b * n + (n + 3) // 4, "step4_fwd": 2 * b * n + (n + 1) // 2,
-              "step4_bwd": 2 * b * n + (n + 1) // 2}
+              "step4_bwd": 2 * b * n + (n + 1) // 2,
+              "swiglu_fwd": 4 * b * n + (n + 3) // 4, "swiglu_bwd": 5 * b * n + (n + 3) // 4}
     act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
     nrm = "msln" if cfg["norm"] == "ln" else "msrms"
     for name, path in libs.items():
@@ -103,6 +105,11 @@ def main():
                                                    codes4.data_ptr(), R, F, DT[dt], sp)
         calls["step4_bwd"] = lambda: L.stepact_bwd(4, ctypes.addressof(lv4), dy.data_ptr(), codes4.data_ptr(),
                                                    dx.data_ptr(), R, F, DT[dt], sp)
+        # fused ReSwiGLU2 on (x as gate, dy as up): h -> y, a -> dx; bwd reads (dy as dh, dy as up, dx as a)
+        calls["swiglu_fwd"] = lambda: L.reswiglu2_fwd(x.data_ptr(), dy.data_ptr(), y.data_ptr(), dx.data_ptr(),
+                                                      codes.data_ptr(), R, F, DT[dt], sp)
+        calls["swiglu_bwd"] = lambda: L.reswiglu2_bwd(y.data_ptr(), dy.data_ptr(), dx.data_ptr(), codes.data_ptr(),
+                                                      x2.data_ptr(), y2.data_ptr(), R, F, DT[dt], sp)
         calls["act_fwd"]()
         calls["norm_fwd"]()
         calls["step4_fwd"]()
