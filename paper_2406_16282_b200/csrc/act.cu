@@ -209,13 +209,15 @@ struct ActFwdLutOp {
   static constexpr bool kTab16 = true;
   static constexpr int W = LMBP_LUT_W, U = LMBP_LUT_U, S = LMBP_LUT_S, kIn = 1, kCodeIn = 0, kCodeOut = 2;
   __device__ static const uint16_t *tab16() { return lut16<T, A>(); }
-  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p, uint32_t tab) {
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const EwParams &p, Tabs tb) {
     const uint32_t c = codes_vec_16<T, A>(v[0]);
+    const uint32_t tab = tb.y;
     st_stream(p.out[0] + i, make_uint4(tab16_pair(tab, v[0].x), tab16_pair(tab, v[0].y), tab16_pair(tab, v[0].z),
                                        tab16_pair(tab, v[0].w)));
     return c;
   }
-  __device__ static void tail(const EwParams &p, uint32_t tab) {
+  __device__ static void tail(const EwParams &p, Tabs tb) {
+    const uint32_t tab = tb.y;
     const int64_t j0 = p.nvec * 8;
     if (j0 >= p.n) return;
     const T *x = reinterpret_cast<const T *>(p.in[0]);

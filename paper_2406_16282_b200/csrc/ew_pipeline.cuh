@@ -60,8 +60,24 @@ template <class Op, class = void> struct Tab16Of { static constexpr bool value =
 template <class Op> struct Tab16Of<Op, std::void_t<decltype(Op::kTab16)>> { static constexpr bool value = Op::kTab16; };
 constexpr uint32_t kTab16Bytes = 65536 * 2;
 
+// Optional per-CTA code table (the k-bit step forwards, stepact.cu): an Op
+// with `static constexpr bool kCtab = true` gets 64 KB of shared memory after
+// the 16-bit table, which its consumer threads fill at CTA start through
+// `__device__ static void fill_ctab(uint8_t *ctab, const Params &, int tid,
+// int nthreads)` (a named barrier among the consumers follows; the producer
+// starts streaming tiles meanwhile).
+template <class Op, class = void> struct CtabOf { static constexpr bool value = false; };
+template <class Op> struct CtabOf<Op, std::void_t<decltype(Op::kCtab)>> { static constexpr bool value = Op::kCtab; };
+constexpr uint32_t kCtabBytes = 65536;
+
+// Shared-window addresses of the tables an Op's apply() / tail() receive.
+struct Tabs {
+  uint32_t y;     // 16-bit output table (Tab16Of)
+  uint32_t code;  // byte-per-pattern code table (CtabOf)
+};
+
 template <class Op> struct EwShape {
-  static constexpr size_t kTabBytes = Tab16Of<Op>::value ? kTab16Bytes : 0;
+  static constexpr size_t kTabBytes = (Tab16Of<Op>::value ? kTab16Bytes : 0) + (CtabOf<Op>::value ? kCtabBytes : 0);
   static constexpr int kTile = Op::W * 32 * Op::U;  // vectors per tile
   static constexpr int kThreads = (Op::W + 1) * 32;
   static constexpr size_t kStageBytes = (size_t)Op::kIn * kTile * 16 + (size_t)Op::kCodeIn * kTile;
@@ -123,9 +139,9 @@ template <class Op> struct LutOf<Op, std::void_t<decltype(Op::kLut)>> { static c
 
 template <class Op, class P, int NIN>
 __device__ __forceinline__ uint32_t apply_op(const uint4 (&v)[NIN], uint32_t c, int64_t i, const P &p,
-                                             const float *lut, uint32_t tab) {
+                                             const float *lut, Tabs tab) {
   if constexpr (LutOf<Op>::value > 0) return Op::apply(v, c, i, p, lut);
-  else if constexpr (Tab16Of<Op>::value) return Op::apply(v, c, i, p, tab);
+  else if constexpr (Tab16Of<Op>::value || CtabOf<Op>::value) return Op::apply(v, c, i, p, tab);
   else return Op::apply(v, c, i, p);
 }
 
@@ -151,6 +167,11 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 // Two packed 16-bit inputs -> two packed 16-bit table outputs.
 // The halves are extracted with PRMT so each address is PRMT + LEA (2 issue
 // slots; written as shifts and masks ptxas emits IADD + LOP3 + IADD).
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(addr));
+  return r;
+}
 __device__ __forceinline__ uint32_t tab16_pair(uint32_t tab, uint32_t w) {
   const uint32_t lo = lds_u16(tab + 2u * __byte_perm(w, 0u, 0x4410));
   const uint32_t hi = lds_u16(tab + 2u * __byte_perm(w, 0u, 0x4432));
@@ -162,7 +183,8 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
   extern __shared__ __align__(128) uint8_t smem_all[];
   using Sh = EwShape<Op>;
   constexpr int W = Op::W, U = Op::U, S = Op::S, NIN = Op::kIn, TILE = Sh::kTile;
-  const uint32_t tab = smem_u32(smem_all);                  // the 16-bit table (when Tab16Of<Op>)
+  constexpr size_t kYTab = Tab16Of<Op>::value ? kTab16Bytes : 0;
+  const Tabs tab{smem_u32(smem_all), smem_u32(smem_all + kYTab)};  // [y table][code table]
   uint8_t *smem = smem_all + Sh::kTabBytes;                 // stages
   uint8_t *cstage = smem + (size_t)S * Sh::kStageBytes;  // codes staging, one slice per warp
   uint64_t *full = reinterpret_cast<uint64_t *>(cstage + Sh::kCodeStage);
@@ -246,6 +268,10 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
     return;
   }
 
+  if constexpr (CtabOf<Op>::value) {
+    Op::fill_ctab(smem_all + kYTab, p, threadIdx.x, W * 32);
+    asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");  // consumers only
+  }
   if constexpr (Tab16Of<Op>::value) mbar_wait(tab_bar, 0);
   for (int k = 0;; ++k) {
     const int s = k % S;
@@ -268,7 +294,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         put_code<Op::kCodeOut>(p.codes_out, i, co);
       }
       if (threadIdx.x == 0) {
-        if constexpr (Tab16Of<Op>::value) Op::tail(p, tab);
+        if constexpr (Tab16Of<Op>::value || CtabOf<Op>::value) Op::tail(p, tab);
         else Op::tail(p);
       }
       continue;

@@ -235,6 +235,114 @@ __device__ __forceinline__ uint32_t step_codes_vec(const uint4 &r, const float *
   return W;
 }
 
+// ---------------------------------------------------------------------------
+// Per-CTA code table for k >= 3 on 16-bit types: the code of every 16-bit
+// pattern, one byte each (64 KB of shared memory), so an element's code is
+// PRMT + IADD + LDS.U8 instead of the k-level compare / mux tree (11 LOP3 per
+// pair at k = 4, the ALU-bound part of the forward, DESIGN 5.6).  The table
+// depends on the runtime thresholds, so the consumers fill it at CTA start
+// (the producer streams the first tiles meanwhile).  Filling walks the two
+// monotone halves of the pattern space: for p < 0x8000, x grows with p and
+// x > t <=> p > A(t); for p >= 0x8000, x falls with p and x > t <=> p < B(t),
+// with A(t) = -1, B(t) = bits(t) for t < 0 and A(t) = bits(t) & 0x7fff,
+// B(t) = 0 otherwise (t = RD_T(c), exact, reading R2); NaN patterns get 0.
+// A chunk of patterns is written a word (4 codes) at a time while no key
+// falls inside the word, else recounted pattern by pattern.
+// ---------------------------------------------------------------------------
+template <typename T> struct Pat16;
+template <> struct Pat16<__nv_bfloat16> { static constexpr int kInf = 0x7F80; };
+template <> struct Pat16<__half> { static constexpr int kInf = 0x7C00; };
+
+#ifndef LMBP_CTAB_CHUNK
+#define LMBP_CTAB_CHUNK 64
+#endif
+
+template <typename T, int K>
+__device__ __forceinline__ void fill_code_table(uint8_t *ctab, const StepTable &tab, int tid, int nthr) {
+  constexpr int M = (1 << K) - 1;
+  __shared__ int sA[16], sB[16];
+  if (tid < M) {
+    const int tb = (int)(tab.thr2[tid] & 0xffffu);
+    const bool negt = (tb & 0x8000) && (tb & 0x7fff);  // strictly negative (-0 acts as +0)
+    sA[tid] = negt ? -1 : (tb & 0x7fff);
+    sB[tid] = negt ? tb : 0;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  auto recount = [&](int q) -> int {
+    int c = 0;
+    if (q < 0x8000) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) c += sA[j] < q;
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) c += sB[j] > q;
+    }
+    return c;
+  };
+  constexpr int CH = LMBP_CTAB_CHUNK;
+  static_assert(CH % 16 == 0, "chunks are written as 16-byte vectors");
+  for (int ch = tid; ch < 65536 / CH; ch += nthr) {
+    const int p0 = ch * CH;
+    const bool neg = p0 >= 0x8000;
+    const int nan_lo = (neg ? (0x8000 | Pat16<T>::kInf) : Pat16<T>::kInf) + 1;  // first NaN pattern of the half
+    int code = recount(p0);
+    // the code is monotone within a half: equal codes at both ends = constant chunk
+    if (p0 + CH - 1 < nan_lo && recount(p0 + CH - 1) == code) {
+      const uint32_t w = (uint32_t)code * 0x01010101u;
+#pragma unroll
+      for (int q = 0; q < CH; q += 16) *reinterpret_cast<uint4 *>(ctab + p0 + q) = make_uint4(w, w, w, w);
+      continue;
+    }
+    for (int e = 0; e < CH; e += 4) {  // a key (or the NaN boundary) falls inside: word by word
+      const int pe = p0 + e;
+      bool fast = pe + 3 < nan_lo;
+      if (!neg) fast = fast && (code == M || pe + 4 <= sA[code]);
+      else fast = fast && (code == 0 || pe + 4 < sB[code - 1]);
+      uint32_t word;
+      if (fast) {
+        word = (uint32_t)code * 0x01010101u;
+      } else {
+        word = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int pq = pe + q;
+          const uint32_t c = pq >= nan_lo ? 0u : (uint32_t)recount(pq);
+          word |= c << (8 * q);
+        }
+        code = recount(pe + 4 < 65536 ? pe + 4 : pe);
+      }
+      *reinterpret_cast<uint32_t *>(ctab + pe) = word;
+    }
+  }
+}
+
+// Codes of one 16-byte vector (8 16-bit elements) from the code table.
+template <int K>
+__device__ __forceinline__ uint32_t ctab_codes_vec(const uint4 &v, uint32_t ctab) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t W = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t lo = lds_u8(ctab + __byte_perm(w[j], 0u, 0x4410));
+    const uint32_t hi = lds_u8(ctab + __byte_perm(w[j], 0u, 0x4432));
+    W |= (lo | (hi << K)) << (2 * K * j);
+  }
+  return W;
+}
+
+// Shapes with tables: GELU (128 KB y table + 64 KB code table) fits one CTA
+// per SM with 8 KB tiles x 3 stages; SiLU (64 KB code table) two CTAs per SM.
+#ifndef LMBP_STEPC_W
+#define LMBP_STEPC_W 12
+#define LMBP_STEPC_U 2
+#define LMBP_STEPC_S 3
+#endif
+#ifndef LMBP_STEPCG_W
+#define LMBP_STEPCG_W 16
+#define LMBP_STEPCG_U 1
+#define LMBP_STEPCG_S 3
+#endif
+
 template <typename T, int A, bool kPrecise, int K>
 struct StepFwdOp {
   using Params = StepEwParams;
@@ -252,15 +360,30 @@ struct StepFwdOp {
 #else
   static constexpr bool kTab16 = false;
 #endif
+#ifndef LMBP_NO_CTAB
+  // the code table where the compare / mux tree is the ALU-bound part: SiLU
+  // (GELU on 16-bit types already holds the 128 KB y table; both tables leave
+  // one CTA per SM with 8 KB tiles, measured slower, profiles/r02/sweep40)
+  static constexpr bool kCtab = sizeof(T) == 2 && K >= 3 && !kTab16;
+#else
+  static constexpr bool kCtab = false;
+#endif
   __device__ static const uint16_t *tab16() {
     if constexpr (kUseLut<T, A>) return lut16<T, A>();
     else return nullptr;
   }
-  static constexpr int kMinBlocks = kTab16 ? 0 : K == 4 ? (k16 ? LMBP_STEP_MINB4 : LMBP_STEP_MINB4_F32) : 0;
+  __device__ static void fill_ctab(uint8_t *ctab, const StepEwParams &p, int tid, int nthr) {
+    if constexpr (kCtab) fill_code_table<T, K>(ctab, p.tab, tid, nthr);
+  }
+  static constexpr int kMinBlocks =
+      (kTab16 || kCtab) ? 0 : K == 4 ? (k16 ? LMBP_STEP_MINB4 : LMBP_STEP_MINB4_F32) : 0;
   static constexpr int kVecT = Traits<T>::kVec;
-  static constexpr int W = kTab16 ? LMBP_STEP_W : K == 4 && k16 ? LMBP_STEP4_W : LMBP_STEP_W, U = LMBP_STEP_U,
-                       S = kTab16 ? LMBP_STEP_S : K == 4 && k16 ? LMBP_STEP4_S : LMBP_STEP_S, kIn = 1, kCodeIn = 0,
-                       kCodeOut = kVecT * K / 8;
+  static constexpr int W = kCtab ? (kTab16 ? LMBP_STEPCG_W : LMBP_STEPC_W)
+                                 : kTab16 ? LMBP_STEP_W : K == 4 && k16 ? LMBP_STEP4_W : LMBP_STEP_W,
+                       U = kCtab ? (kTab16 ? LMBP_STEPCG_U : LMBP_STEPC_U) : LMBP_STEP_U,
+                       S = kCtab ? (kTab16 ? LMBP_STEPCG_S : LMBP_STEPC_S)
+                                 : kTab16 ? LMBP_STEP_S : K == 4 && k16 ? LMBP_STEP4_S : LMBP_STEP_S,
+                       kIn = 1, kCodeIn = 0, kCodeOut = kVecT * K / 8;
   __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p) {
     float f[kVecT];
     Vec<T>::unpack(v[0], f);
@@ -274,14 +397,28 @@ struct StepFwdOp {
     st_stream(p.out[0] + i, Vec<T>::pack(f));
     return w;
   }
-  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p, uint32_t tab) {
-    float f[kVecT];  // unused by the 16-bit code search
-    const uint32_t w = step_codes_vec<T, K>(v[0], f, p.tab);
-    st_stream(p.out[0] + i, make_uint4(tab16_pair(tab, v[0].x), tab16_pair(tab, v[0].y), tab16_pair(tab, v[0].z),
-                                       tab16_pair(tab, v[0].w)));
+  // 16-bit types with a y table and/or a code table.
+  __device__ static uint32_t apply(const uint4 (&v)[1], uint32_t, int64_t i, const StepEwParams &p, Tabs tb) {
+    float f[kVecT];
+    uint32_t w;
+    if constexpr (kCtab) w = ctab_codes_vec<K>(v[0], tb.code);
+    else w = step_codes_vec<T, K>(v[0], f, p.tab);  // (f unused for 16-bit types)
+    if constexpr (kTab16) {
+      st_stream(p.out[0] + i, make_uint4(tab16_pair(tb.y, v[0].x), tab16_pair(tb.y, v[0].y),
+                                         tab16_pair(tb.y, v[0].z), tab16_pair(tb.y, v[0].w)));
+    } else {
+      Vec<T>::unpack(v[0], f);
+#pragma unroll
+      for (int e = 0; e < kVecT; e += 2) {
+        const float2 r = act2_f<A, kPrecise>(make_float2(f[e], f[e + 1]));
+        f[e] = r.x;
+        f[e + 1] = r.y;
+      }
+      st_stream(p.out[0] + i, Vec<T>::pack(f));
+    }
     return w;
   }
-  __device__ static void tail(const StepEwParams &p, uint32_t tab = 0) {
+  __device__ static void tail(const StepEwParams &p, Tabs tb = Tabs{0, 0}) {
     const int64_t j0 = p.nvec * kVecT;
     if (j0 >= p.n) return;
     const T *x = reinterpret_cast<const T *>(p.in[0]);
@@ -291,7 +428,7 @@ struct StepFwdOp {
       const float f = to_f32<T>(x[j]);
       w |= step_code<K>(f, p.tab.thr) << (K * (j - j0));
       if constexpr (kTab16) {
-        const uint16_t b = (uint16_t)lds_u16(tab + 2u * reinterpret_cast<const uint16_t *>(x)[j]);
+        const uint16_t b = (uint16_t)lds_u16(tb.y + 2u * reinterpret_cast<const uint16_t *>(x)[j]);
         y[j] = *reinterpret_cast<const T *>(&b);
       } else {
         y[j] = from_f32<T>(act_f<A, kPrecise>(f));

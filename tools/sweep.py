@@ -68,6 +68,9 @@ def main():
     thr2 = (ctypes.c_double * 3)(-3.1858810036855245, -0.001178821281161997, 3.190832613414926)
     lv2 = (ctypes.c_double * 4)(0.0, -0.04922261145617846, 1.0487405950855513, 1.0)
     thr4 = (ctypes.c_double * 15)(*[-3.0 + 0.4 * i for i in range(15)])
+    thr3 = (ctypes.c_double * 7)(*[-3.0 + 1.0 * i for i in range(7)])
+    lv3 = (ctypes.c_double * 8)(*[i / 7 for i in range(8)])
+    codes3 = torch.empty((R * F * 3 + 7) // 8, dtype=torch.uint8, device=dev)
     lv4 = (ctypes.c_double * 16)(*[i / 15 for i in range(16)])
     xn = synth.norm_input(R, H, dt, device=dev)
     gn = synth.grad_input(R, H, dt, device=dev)
@@ -82,7 +85,8 @@ def main():
     nbytes = {"ncopy": 2 * b * R * H, "copy": 2 * b * n, "act_fwd": 2 * b * n + (n + 3) // 4, "act_bwd": 2 * b * n + (n + 3) // 4,
               "norm_fwd": (2 * b * H + 4) * R, "norm_bwd": (3 * b * H + 4) * R,
               "step2_fwd": 2 * b * n + (n + 3) // 4, "step4_fwd": 2 * b * n + (n + 1) // 2,
-              "step4_bwd": 2 * b * n + (n + 1) // 2,
+              "step4_bwd": 2 * b * n + (n + 1) // 2, "step3_fwd": 2 * b * n + (3 * n + 7) // 8,
+              "step3_bwd": 2 * b * n + (3 * n + 7) // 8,
               "swiglu_fwd": 4 * b * n + (n + 3) // 4, "swiglu_bwd": 5 * b * n + (n + 3) // 4}
     act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
     nrm = "msln" if cfg["norm"] == "ln" else "msrms"
@@ -103,6 +107,10 @@ def main():
                                                    codes.data_ptr(), R, F, DT[dt], sp)
         calls["step4_fwd"] = lambda: L.stepact_fwd(ak, 4, ctypes.addressof(thr4), x.data_ptr(), y.data_ptr(),
                                                    codes4.data_ptr(), R, F, DT[dt], sp)
+        calls["step3_fwd"] = lambda: L.stepact_fwd(ak, 3, ctypes.addressof(thr3), x.data_ptr(), y.data_ptr(),
+                                                   codes3.data_ptr(), R, F, DT[dt], sp)
+        calls["step3_bwd"] = lambda: L.stepact_bwd(3, ctypes.addressof(lv3), dy.data_ptr(), codes3.data_ptr(),
+                                                   dx.data_ptr(), R, F, DT[dt], sp)
         calls["step4_bwd"] = lambda: L.stepact_bwd(4, ctypes.addressof(lv4), dy.data_ptr(), codes4.data_ptr(),
                                                    dx.data_ptr(), R, F, DT[dt], sp)
         # fused ReSwiGLU2 on (x as gate, dy as up): h -> y, a -> dx; bwd reads (dy as dh, dy as up, dx as a)
