@@ -21,8 +21,13 @@ for dt in ("f32", "bf16", "f16"):
         h, a, c = P.reswiglu2_fwd(x, dy)
         P.reswiglu2_bwd(dy, dy, a, c)
         for k, thr, lv in ((1, [0.0], [0.0, 1.0]), (2, tables.REGELU2["c"], tables.levels(tables.REGELU2)),
+                           (3, [-3.0 + 1.0 * i for i in range(7)], [i / 7 for i in range(8)]),
                            (4, [-3.0 + 0.4 * i for i in range(15)], [i / 15 for i in range(16)])):
-            y, c = P.stepact_fwd(x, "gelu", k, thr)
+            for act in ("gelu", "silu"):            # GELU 16-bit: y table; SiLU 16-bit k >= 3: code table
+                y, c = P.stepact_fwd(x, act, k, thr)
+                P.stepact_bwd(dy, c, k, lv)
+            cb = torch.empty(c.numel() + 1, dtype=torch.uint8, device=dev)   # misaligned codes: simple kernels
+            y, c = P.stepact_fwd(x, "silu", k, thr, codes=cb[1:])
             P.stepact_bwd(dy, c, k, lv)
     for (R, H) in ((3, 7), (33, 768), (9, 4096), (5, 5120), (2, 40000)):
         xn = synth.norm_input(R, H, dt).to(dev)
