@@ -64,6 +64,9 @@ def parse(argv=None):
                     help="config of the row-sharded strong-scaling key (north_star: C5)")
     ap.add_argument("--strong-steps", type=int, default=10)
     ap.add_argument("--no-strong", action="store_true", help="skip the strong-scaling (row-sharded C5) key")
+    ap.add_argument("--nvtx", action="store_true",
+                    help="wrap every kernel launch in an NVTX range named after the 8(a) row "
+                         "(e.g. ncu --nvtx --nvtx-include act_fwd/)")
     return ap.parse_args(argv)
 
 
@@ -605,9 +608,9 @@ class Workload:
     four launches of one step (norm fwd -> act fwd -> act bwd ->
     norm bwd) through the C-ABI binding."""
 
-    def __init__(self, P, cfg, row0, R, dev, stream, eps):
+    def __init__(self, P, cfg, row0, R, dev, stream, eps, nvtx=False):
         F, H, dt = cfg["F"], cfg["H"], cfg["dtype"]
-        self.cfg, self.R, self.dev, self.stream, self.eps = cfg, R, dev, stream, eps
+        self.cfg, self.R, self.dev, self.stream, self.eps, self.nvtx = cfg, R, dev, stream, eps, nvtx
         self.act_fwd, self.act_bwd = ((P.regelu2_fwd, P.regelu2_bwd) if cfg["act"] == "gelu"
                                       else (P.resilu2_fwd, P.resilu2_bwd))
         self.norm_fwd, self.norm_bwd = ((P.msln_fwd, P.msln_bwd) if cfg["norm"] == "ln"
@@ -634,7 +637,11 @@ class Workload:
             sink.copy_(flush.sum())                    # evict L2 by reading 2 x L2 (outside the events)
             if evs is not None:
                 evs[2 * i].record(self.stream)
+            if self.nvtx:
+                torch.cuda.nvtx.range_push(k)
             self.launch[k]()
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
             if evs is not None:
                 evs[2 * i + 1].record(self.stream)
 
@@ -743,7 +750,7 @@ def main(argv=None):
     stream = torch.cuda.current_stream(dev)
     cdev = dev if backend == "nccl" else torch.device("cpu")
 
-    w = Workload(P, cfg, row0, R, dev, stream, args.eps)
+    w = Workload(P, cfg, row0, R, dev, stream, args.eps, nvtx=args.nvtx)
     x, dy, xn, gn, y, dx = w.x, w.dy, w.xn, w.gn, w.y, w.dx
     codes, yn, dxn, rstd = w.codes, w.yn, w.dxn, w.rstd
     norm_fwd, norm_bwd, act_fwd, act_bwd = w.norm_fwd, w.norm_bwd, w.act_fwd, w.act_bwd
