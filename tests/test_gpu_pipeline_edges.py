@@ -9,7 +9,7 @@ import torch
 import oracle
 import synth
 import paper_2406_16282_b200 as P
-from test_gpu_parity import DEV, check_act_bwd, check_act_fwd, st
+from test_gpu_parity import DEV, check_act_bwd, check_act_fwd, st, ulp_dist
 
 pytestmark = pytest.mark.gpu
 
@@ -65,3 +65,34 @@ def test_concurrent_streams_match_serial():
     torch.cuda.synchronize()
     for (y0, c0), (y1, c1) in zip(serial, outs):
         assert torch.equal(c0, c1) and torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("kind", ["gelu", "silu"])
+def test_stepact_tile_boundaries(kind, k):
+    """k-bit forwards on 16-bit types at and around their tile sizes: the
+    GELU table shape (1024 vectors), the SiLU code-table shape (768 vectors),
+    the backward (1536); codes bytewise and dx bitwise against the oracle."""
+    m = (1 << k) - 1
+    thr = [-3.0 + 6.0 * i / (m - 1) for i in range(m)]
+    lv = [(-1) ** i * (i + 1) / m for i in range(m + 1)]
+    out = []
+    for tile in (768, 1024, 1536):
+        for j in (1, 2):
+            base = tile * 8 * j
+            out += [base, base + 8, base + 1, base - 1, base - 8, base + 3 * 8 + 5]
+    for n in sorted(set(out)):
+        x = synth.act_input(1, n, "bf16", mode="coverage")
+        dy = synth.grad_input(1, n, "bf16")
+        y, codes = P.stepact_fwd(x.to(DEV), kind, k, thr)
+        dx = P.stepact_bwd(dy.to(DEV), codes, k, lv)
+        torch.cuda.synchronize()
+        x64 = oracle.decode(st(x), "bf16")
+        y_ref, c_ref = oracle.stepact_fwd(kind, k, thr, x64)
+        assert np.array_equal(codes.cpu().numpy(), c_ref), (kind, k, n)
+        want = oracle.stepact_bwd_contract(k, lv, c_ref, st(dy), "bf16")
+        assert np.array_equal(st(dx).view(np.uint16), want.view(np.uint16)), (kind, k, n)
+        yr = oracle.round_to(y_ref.reshape(-1), "bf16")
+        d = ulp_dist(st(y).reshape(-1), yr, "bf16")
+        finite = np.isfinite(x64.reshape(-1))
+        assert d[finite].max() <= 1, (kind, k, n)
