@@ -153,6 +153,30 @@ LMBP_API int msrms_bwd(const void *dy, const void *y, const float *rstd, void *d
               int64_t cols, int dtype, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Mixed-precision MS-LN / MS-RMSNorm: fp32 residual stream, 16-bit output.
+ * Under AMP the paper's norms run in fp32 while the linears run in 16 bits
+ * (Fig. 5 / 6 captions).  Sharing y with the next linear
+ * (Prop. 5.1 condition 3) needs y in that linear's input dtype, so:
+ * Forward:  x: fp32 [rows, cols]; y: [rows, cols] in `dtype` (LMBP_BF16 or
+ *           LMBP_F16), y = RN_dtype((x - mu) rstd) (RMS: x rstd), statistics
+ *           in fp32 exactly as msln_fwd / msrms_fwd; rstd: fp32 [rows].
+ * Backward: dy, y: [rows, cols] in `dtype`; rstd: fp32 [rows]; dx: fp32
+ *           [rows, cols] output: rstd (dy - mean dy - y mean(dy y)) (RMS
+ *           without mean dy), not rounded to 16 bits.
+ * dtype LMBP_F32 (or unknown) -> LMBP_ERR_DTYPE (use msln_* / msrms_*).  No
+ * aliasing between the fp32 and 16-bit tensors.  Other arguments, errors and
+ * alignment rules as msln_* (misaligned or cols % 8 != 0: a scalar path).
+ * ------------------------------------------------------------------------- */
+LMBP_API int msln_fwd_mixed(const float *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                            int dtype, void *stream);
+LMBP_API int msln_bwd_mixed(const void *dy, const void *y, const float *rstd, float *dx, int64_t rows,
+                            int64_t cols, int dtype, void *stream);
+LMBP_API int msrms_fwd_mixed(const float *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,
+                             int dtype, void *stream);
+LMBP_API int msrms_bwd_mixed(const void *dy, const void *y, const float *rstd, float *dx, int64_t rows,
+                             int64_t cols, int dtype, void *stream);
+
+/* ---------------------------------------------------------------------------
  * ReSwiGLU2: fused LLaMA gate h = SiLU(gate) * up with ReSiLU2's backward
  * (SwiGLU; ReSiLU2).  Semantics are
  * exactly those of the unfused composition resilu2_fwd -> elementwise mul

@@ -8,11 +8,12 @@ fallback.
 """
 from .ops import (codes_bytes, msln_bwd, msln_fwd, msrms_bwd, msrms_fwd, regelu2_bwd, regelu2_fwd,  # noqa: F401
                   resilu2_bwd, resilu2_fwd, reswiglu2_bwd, reswiglu2_fwd, step_table, stepact_fwd, stepact_bwd,
-                  codes_bytes_k)
+                  codes_bytes_k, msln_fwd_mixed, msln_bwd_mixed, msrms_fwd_mixed, msrms_bwd_mixed)
 from .modules import (MSLayerNorm, MSLayerNormFn, MSRMSNorm, MSRMSNormFn, ReGELU2, ReGELU2Fn, ReSiLU2,  # noqa: F401
                       ReSiLU2Fn, ReSwiGLU2, ReSwiGLU2Fn, saved_bytes)
 
 __all__ = ["regelu2_fwd", "regelu2_bwd", "resilu2_fwd", "resilu2_bwd", "msln_fwd", "msln_bwd", "msrms_fwd",
-           "msrms_bwd", "reswiglu2_fwd", "reswiglu2_bwd", "stepact_fwd", "stepact_bwd", "codes_bytes_k", "codes_bytes", "step_table", "ReGELU2", "ReSiLU2",
+           "msrms_bwd", "reswiglu2_fwd", "reswiglu2_bwd", "stepact_fwd", "stepact_bwd", "codes_bytes_k", "codes_bytes", "step_table",
+           "msln_fwd_mixed", "msln_bwd_mixed", "msrms_fwd_mixed", "msrms_bwd_mixed", "ReGELU2", "ReSiLU2",
            "ReSwiGLU2", "MSLayerNorm", "MSRMSNorm", "ReGELU2Fn", "ReSiLU2Fn", "ReSwiGLU2Fn", "MSLayerNormFn",
            "MSRMSNormFn", "saved_bytes"]

@@ -28,6 +28,10 @@ SIGNATURES = {
     "msln_bwd": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "msrms_fwd": (_i32, [_p, _p, _p, _i64, _i64, _f32, _i32, _p]),
     "msrms_bwd": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "msln_fwd_mixed": (_i32, [_p, _p, _p, _i64, _i64, _f32, _i32, _p]),
+    "msln_bwd_mixed": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
+    "msrms_fwd_mixed": (_i32, [_p, _p, _p, _i64, _i64, _f32, _i32, _p]),
+    "msrms_bwd_mixed": (_i32, [_p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "reswiglu2_fwd": (_i32, [_p, _p, _p, _p, _p, _i64, _i64, _i32, _p]),
     "lmbp_codes_bytes_k": (ctypes.c_size_t, [_i64, _i32]),
     "stepact_fwd": (_i32, [_i32, _i32, _p, _p, _p, _p, _i64, _i64, _i32, _p]),

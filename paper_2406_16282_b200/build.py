@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "liblmbp.so")
-SOURCES = ["abi.cu", "act.cu", "norm.cu", "swiglu.cu", "stepact.cu", "fit.cu"]
+SOURCES = ["abi.cu", "act.cu", "norm.cu", "norm_mixed.cu", "swiglu.cu", "stepact.cu", "fit.cu"]
 HEADERS = ["common.cuh", "constants.cuh", "kernels.h", "act_math.cuh", "act_lut.cuh", "ew_pipeline.cuh",
            os.path.join("..", "..", "include", "lmbp.h"), os.path.join("..", "_obj", "act_lut.inc")]
 

@@ -60,6 +60,29 @@ static int norm_fwd_entry(int kind, const void *x, void *y, float *rstd, int64_t
   return status_of(norm_fwd(kind, dtype, x, y, rstd, rows, cols, eps, static_cast<cudaStream_t>(stream)));
 }
 
+static int mixed_dtype(int dtype) { return (dtype == LMBP_BF16 || dtype == LMBP_F16) ? LMBP_OK : LMBP_ERR_DTYPE; }
+
+static int norm_fwd_mixed_entry(int kind, const float *x, void *y, float *rstd, int64_t rows, int64_t cols,
+                                float eps, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = mixed_dtype(dtype)) != LMBP_OK) return st;
+  if (!(eps > 0.0f) || !std::isfinite(eps)) return LMBP_ERR_EPS;
+  if (rows == 0) return LMBP_OK;
+  if (!x || !y || !rstd) return LMBP_ERR_NULLPTR;
+  return status_of(norm_fwd_mixed(kind, dtype, x, y, rstd, rows, cols, eps, static_cast<cudaStream_t>(stream)));
+}
+
+static int norm_bwd_mixed_entry(int kind, const void *dy, const void *y, const float *rstd, float *dx, int64_t rows,
+                                int64_t cols, int dtype, void *stream) {
+  int st = check_shape(rows, cols);
+  if (st != LMBP_OK) return st;
+  if ((st = mixed_dtype(dtype)) != LMBP_OK) return st;
+  if (rows == 0) return LMBP_OK;
+  if (!dy || !y || !rstd || !dx) return LMBP_ERR_NULLPTR;
+  return status_of(norm_bwd_mixed(kind, dtype, dy, y, rstd, dx, rows, cols, static_cast<cudaStream_t>(stream)));
+}
+
 static int norm_bwd_entry(int kind, const void *dy, const void *y, const float *rstd, void *dx, int64_t rows,
                           int64_t cols, int dtype, void *stream) {
   int st = check_shape(rows, cols);
@@ -232,6 +255,23 @@ int msrms_fwd(const void *x, void *y, float *rstd, int64_t rows, int64_t cols, f
 int msrms_bwd(const void *dy, const void *y, const float *rstd, void *dx, int64_t rows, int64_t cols, int dtype,
               void *stream) {
   return lmbp::norm_bwd_entry(lmbp::kNormRMS, dy, y, rstd, dx, rows, cols, dtype, stream);
+}
+
+int msln_fwd_mixed(const float *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps, int dtype,
+                   void *stream) {
+  return lmbp::norm_fwd_mixed_entry(lmbp::kNormLN, x, y, rstd, rows, cols, eps, dtype, stream);
+}
+int msln_bwd_mixed(const void *dy, const void *y, const float *rstd, float *dx, int64_t rows, int64_t cols, int dtype,
+                   void *stream) {
+  return lmbp::norm_bwd_mixed_entry(lmbp::kNormLN, dy, y, rstd, dx, rows, cols, dtype, stream);
+}
+int msrms_fwd_mixed(const float *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps, int dtype,
+                    void *stream) {
+  return lmbp::norm_fwd_mixed_entry(lmbp::kNormRMS, x, y, rstd, rows, cols, eps, dtype, stream);
+}
+int msrms_bwd_mixed(const void *dy, const void *y, const float *rstd, float *dx, int64_t rows, int64_t cols,
+                    int dtype, void *stream) {
+  return lmbp::norm_bwd_mixed_entry(lmbp::kNormRMS, dy, y, rstd, dx, rows, cols, dtype, stream);
 }
 
 int reswiglu2_fwd(const void *gate, const void *up, void *h, void *a, uint8_t *codes, int64_t rows, int64_t cols,

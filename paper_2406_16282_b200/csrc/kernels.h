@@ -17,6 +17,11 @@ cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, i
                      float eps, cudaStream_t s);
 cudaError_t norm_bwd(int kind, int dtype, const void *dy, const void *y, const float *rstd, void *dx,
                      int64_t rows, int64_t cols, cudaStream_t s);
+// fp32 residual stream, 16-bit y / dy (norm_mixed.cu); dtype: 1 bf16, 2 fp16
+cudaError_t norm_fwd_mixed(int kind, int dtype, const float *x, void *y, float *rstd, int64_t rows, int64_t cols,
+                           float eps, cudaStream_t s);
+cudaError_t norm_bwd_mixed(int kind, int dtype, const void *dy, const void *y, const float *rstd, float *dx,
+                           int64_t rows, int64_t cols, cudaStream_t s);
 
 struct StepTable;  // common.cuh
 cudaError_t stepact_fwd(int act, int dtype, const StepTable &t, const void *x, void *y, uint8_t *codes, int64_t n,

@@ -68,6 +68,25 @@ class MSRMSNormFn(torch.autograd.Function):
         return ops.msrms_bwd(dy.contiguous(), y, rstd), None
 
 
+class MSNormMixedFn(torch.autograd.Function):
+    """fp32 residual x -> 16-bit y (the next linear's input dtype); saves
+    (y, rstd); backward returns the fp32 dx of the residual stream."""
+
+    @staticmethod
+    def forward(ctx, x, eps, out_dtype, ln):
+        fwd = ops.msln_fwd_mixed if ln else ops.msrms_fwd_mixed
+        y, rstd = fwd(x.contiguous(), eps, out_dtype)
+        ctx.save_for_backward(y, rstd)
+        ctx.ln = ln
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        y, rstd = ctx.saved_tensors
+        bwd = ops.msln_bwd_mixed if ctx.ln else ops.msrms_bwd_mixed
+        return bwd(dy.to(y.dtype).contiguous(), y, rstd), None, None, None
+
+
 class ReSwiGLU2Fn(torch.autograd.Function):
     """h = SiLU(gate) * up with ReSiLU2's backward, fused; saves (up, a, codes)
     where a = SiLU(gate) -- 2b + 1/4 bytes per element instead of 3b."""
@@ -101,28 +120,36 @@ class ReSiLU2(torch.nn.Module):
 
 
 class MSLayerNorm(torch.nn.Module):
-    """Affine-free LayerNorm whose backward needs only (y, rstd)."""
+    """Affine-free LayerNorm whose backward needs only (y, rstd).  With
+    ``out_dtype`` (bfloat16 / float16) an fp32 input is normalised straight
+    into that dtype (msln_fwd_mixed: AMP's fp32 norm feeding a 16-bit linear)."""
 
-    def __init__(self, normalized_shape: int, eps: float = 1e-6):
+    def __init__(self, normalized_shape: int, eps: float = 1e-6, out_dtype=None):
         super().__init__()
         self.normalized_shape = int(normalized_shape)
         self.eps = float(eps)
+        self.out_dtype = out_dtype
 
     def forward(self, x):
         if x.shape[-1] != self.normalized_shape:
             raise ValueError("last dimension mismatch")
+        if self.out_dtype is not None and x.dtype == torch.float32 and self.out_dtype != torch.float32:
+            return MSNormMixedFn.apply(x, self.eps, self.out_dtype, True)
         return MSLayerNormFn.apply(x, self.eps)
 
 
 class MSRMSNorm(torch.nn.Module):
-    def __init__(self, normalized_shape: int, eps: float = 1e-6):
+    def __init__(self, normalized_shape: int, eps: float = 1e-6, out_dtype=None):
         super().__init__()
         self.normalized_shape = int(normalized_shape)
         self.eps = float(eps)
+        self.out_dtype = out_dtype
 
     def forward(self, x):
         if x.shape[-1] != self.normalized_shape:
             raise ValueError("last dimension mismatch")
+        if self.out_dtype is not None and x.dtype == torch.float32 and self.out_dtype != torch.float32:
+            return MSNormMixedFn.apply(x, self.eps, self.out_dtype, False)
         return MSRMSNormFn.apply(x, self.eps)
 
 

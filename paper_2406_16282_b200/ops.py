@@ -165,6 +165,57 @@ def msrms_bwd(dy, y, rstd, dx=None, stream=None):
     return _norm_bwd("msrms_bwd", dy, y, rstd, dx, stream)
 
 
+def _norm_fwd_mixed(fn, x, eps, out_dtype, y, rstd, stream):
+    _need(x, "x")
+    if x.dtype != torch.float32:
+        raise ValueError(f"{fn}: x must be float32 (the fp32 residual stream)")
+    if out_dtype not in (torch.bfloat16, torch.float16):
+        raise ValueError(f"{fn}: out_dtype must be bfloat16 or float16")
+    rows, cols = _rc(x)
+    y = torch.empty(x.shape, dtype=out_dtype, device=x.device) if y is None else _need(y, "y")
+    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device) if rstd is None else _need(rstd, "rstd")
+    if y.shape != x.shape or y.dtype != out_dtype or rstd.numel() != rows or rstd.dtype != torch.float32:
+        raise ValueError(f"{fn}: shape/dtype mismatch")
+    _launch(fn, _device(fn, x, y, rstd), stream, x.data_ptr(), y.data_ptr(), rstd.data_ptr(), rows, cols,
+            float(eps), _dtype(y))
+    return y, rstd
+
+
+def _norm_bwd_mixed(fn, dy, y, rstd, dx, stream):
+    for t, nm in ((dy, "dy"), (y, "y"), (rstd, "rstd")):
+        _need(t, nm)
+    if dy.dtype not in (torch.bfloat16, torch.float16) or y.dtype != dy.dtype:
+        raise ValueError(f"{fn}: dy and y must share a 16-bit dtype")
+    rows, cols = _rc(dy)
+    dx = torch.empty(dy.shape, dtype=torch.float32, device=dy.device) if dx is None else _need(dx, "dx")
+    if y.shape != dy.shape or rstd.numel() != rows or rstd.dtype != torch.float32 or dx.shape != dy.shape \
+            or dx.dtype != torch.float32:
+        raise ValueError(f"{fn}: token/shape mismatch (S:L266)")
+    _launch(fn, _device(fn, dy, y, rstd, dx), stream, dy.data_ptr(), y.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+            rows, cols, _dtype(dy))
+    return dx
+
+
+def msln_fwd_mixed(x, eps=1e-6, out_dtype=torch.bfloat16, y=None, rstd=None, stream=None):
+    """MS-LN forward from an fp32 residual stream to a 16-bit y (AMP).  lmbp.h msln_fwd_mixed."""
+    return _norm_fwd_mixed("msln_fwd_mixed", x, eps, out_dtype, y, rstd, stream)
+
+
+def msln_bwd_mixed(dy, y, rstd, dx=None, stream=None):
+    """MS-LN backward: 16-bit (dy, y) + rstd -> fp32 dx.  lmbp.h msln_bwd_mixed."""
+    return _norm_bwd_mixed("msln_bwd_mixed", dy, y, rstd, dx, stream)
+
+
+def msrms_fwd_mixed(x, eps=1e-6, out_dtype=torch.bfloat16, y=None, rstd=None, stream=None):
+    """MS-RMSNorm forward, fp32 x -> 16-bit y.  lmbp.h msrms_fwd_mixed."""
+    return _norm_fwd_mixed("msrms_fwd_mixed", x, eps, out_dtype, y, rstd, stream)
+
+
+def msrms_bwd_mixed(dy, y, rstd, dx=None, stream=None):
+    """MS-RMSNorm backward, 16-bit (dy, y) -> fp32 dx.  lmbp.h msrms_bwd_mixed."""
+    return _norm_bwd_mixed("msrms_bwd_mixed", dy, y, rstd, dx, stream)
+
+
 def step_table(kind: str):
     """The kernels' binary32 (thresholds[3], levels[4]) for 'gelu' / 'silu'."""
     import ctypes

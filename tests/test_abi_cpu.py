@@ -231,3 +231,22 @@ def test_stepact_binding_refuses_wrong_table_lengths():
         ops.stepact_bwd(x, torch.zeros(12, dtype=torch.uint8), 3, [0.0] * 7)
     with pytest.raises(ValueError, match="k must be"):
         ops.stepact_fwd(x, "gelu", 5, [0.0] * 31)
+
+
+def test_mixed_norm_validation_without_device_work():
+    """msln/msrms *_mixed: fp32 residual stream with 16-bit y / dy; an fp32 or
+    unknown `dtype` is refused, eps and pointers validated as msln_*."""
+    L = _lib.lib()
+    S = _lib
+    fake = ctypes.c_void_p(0x1000)
+    for fn in (L.msln_fwd_mixed, L.msrms_fwd_mixed):
+        assert fn(fake, fake, fake, 2, 8, 1e-6, S.LMBP_F32, None) == S.LMBP_ERR_DTYPE
+        assert fn(fake, fake, fake, 2, 8, 1e-6, 7, None) == S.LMBP_ERR_DTYPE
+        assert fn(fake, fake, fake, 2, 8, 0.0, S.LMBP_BF16, None) == S.LMBP_ERR_EPS
+        assert fn(fake, None, fake, 2, 8, 1e-6, S.LMBP_F16, None) == S.LMBP_ERR_NULLPTR
+        assert fn(fake, fake, fake, -1, 8, 1e-6, S.LMBP_BF16, None) == S.LMBP_ERR_SHAPE
+        assert fn(None, None, None, 0, 8, 1e-6, S.LMBP_BF16, None) == S.LMBP_OK
+    for fn in (L.msln_bwd_mixed, L.msrms_bwd_mixed):
+        assert fn(fake, fake, fake, fake, 2, 8, S.LMBP_F32, None) == S.LMBP_ERR_DTYPE
+        assert fn(fake, fake, None, fake, 2, 8, S.LMBP_BF16, None) == S.LMBP_ERR_NULLPTR
+        assert fn(None, None, None, None, 0, 8, S.LMBP_F16, None) == S.LMBP_OK
