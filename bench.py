@@ -446,6 +446,42 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
             "gpu_launches": 2 * iters}
 
 
+def mixed_norm_section(P, cfg, R, dev, stream, flush, sink, peak, eps, iters=20):
+    """Mixed-precision MS norm (fp32 residual in, 16-bit y out; 16-bit dy ->
+    fp32 dx; the AMP layout of Fig. 5 / 6) at the config's [R, H]: us and
+    GB/s of fwd and bwd on their algorithmic bytes."""
+    if cfg["dtype"] == "f32":
+        return None
+    H = cfg["H"]
+    ln = cfg["norm"] == "ln"
+    x = synth.norm_input(R, H, "f32", device=dev)
+    g = synth.grad_input(R, H, cfg["dtype"], device=dev, stream=synth.S_NORM_DY)
+    y = torch.empty(R, H, dtype=synth.TORCH_DTYPES[cfg["dtype"]], device=dev)
+    rstd = torch.empty(R, dtype=torch.float32, device=dev)
+    dx = torch.empty(R, H, dtype=torch.float32, device=dev)
+    fwd, bwd = (P.msln_fwd_mixed, P.msln_bwd_mixed) if ln else (P.msrms_fwd_mixed, P.msrms_bwd_mixed)
+    fns = {"fwd": lambda: fwd(x, eps, y.dtype, y=y, rstd=rstd, stream=stream),
+           "bwd": lambda: bwd(g, y, rstd, dx=dx, stream=stream)}
+    nbytes = {"fwd": (4 * H + 2 * H + 4) * R, "bwd": (2 * 2 * H + 4 + 4 * H) * R}
+    out = {"shape": [R, H], "x": "f32", "y": cfg["dtype"]}
+    for k, fn in fns.items():
+        for _ in range(3):
+            fn()
+        evs = []
+        for _ in range(iters):
+            sink.copy_(flush.sum())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        us = float(np.median([a.elapsed_time(b) * 1e3 for a, b in evs]))
+        out[k] = {"us_median": round(us, 2), "bytes": nbytes[k], "GB/s": round(nbytes[k] / us / 1e3, 1),
+                  "frac": round(nbytes[k] / us / 1e3 / peak, 4)}
+    return out
+
+
 def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     """the table-driven k-bit step activation on the
     config's activation tensor -- k = 2 with the paper's table (bitwise equal
@@ -583,10 +619,12 @@ def block_section(cfg, dev, tunings=("full", "lora_qv", "lora_all", "lora_fa_all
            "unit_bytes": unit, "decoded_model_full_tuning": {k: round(v, 4) for k, v in unit_model(arch, h / c).items()},
            "model_note": "torch SDPA returns [b, n, h, d]: the out-projection's saved input is the attention output "
                          "itself, one unit below the model's separate kernels", "tunings": {}}
-    for t in tunings:
-        blk = Block(arch, c, h, cfg["heads"], tuning=t, dtype=dt, device=dev)
-        te, pe = activation_bytes(blk, x, by_module=True)
-        to, po = activation_bytes(blk.to_ours(), x, by_module=True)
+    x32 = x.detach().float().requires_grad_(True)
+    for t in list(tunings) + ["full_amp"]:
+        amp = t == "full_amp"           # fp32 residual stream, bf16 linears: the mixed MS norms
+        blk = Block(arch, c, h, cfg["heads"], tuning="full" if amp else t, dtype=dt, device=dev, residual_fp32=amp)
+        te, pe = activation_bytes(blk, x32 if amp else x, by_module=True)
+        to, po = activation_bytes(blk.to_ours(), x32 if amp else x, by_module=True)
         out["tunings"][t] = {"exact_units": round(te / unit, 4), "ours_units": round(to / unit, 4),
                              "saved_fraction": round(1 - to / te, 4), "exact_bytes": te, "ours_bytes": to,
                              "norm_shared": [blk.norm_shared(1), blk.norm_shared(2)],
@@ -874,6 +912,7 @@ def main(argv=None):
     swiglu = swiglu_section(P, cfg, x, dy, stream, flush, flush_sink, args) if cfg["act"] == "silu" else None
     block = block_section(cfg, dev) if rank == 0 else None
     step_k = stepact_section(P, cfg, x, dy, stream, flush, flush_sink, peak)
+    mixed = mixed_norm_section(P, cfg, R, dev, stream, flush, flush_sink, peak, args.eps)
     fitter = fitter_section(stream, cpu=(world == 1 and not args.no_cpu_baseline)) if (
         rank == 0 and not args.no_fitter) else None
 
@@ -908,6 +947,7 @@ def main(argv=None):
             "reswiglu2": swiglu,
             "activation_bytes_saved_per_block": block,
             "stepact": step_k,
+            "mixed_norm": mixed,
             "fitter": fitter,
         }
         print(json.dumps(line), flush=True)

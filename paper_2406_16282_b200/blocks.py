@@ -150,7 +150,7 @@ class _NormRefFn(torch.autograd.Function):
     compute dtype), per-row statistics and the affine parameters."""
 
     @staticmethod
-    def forward(ctx, x, alpha, beta, eps, ln, fp32):
+    def forward(ctx, x, alpha, beta, eps, ln, fp32, out_dtype=None):
         xc = x.float() if fp32 else x
         xf = xc.float()
         mu = xf.mean(-1, keepdim=True) if ln else torch.zeros_like(xf[..., :1])
@@ -162,7 +162,8 @@ class _NormRefFn(torch.autograd.Function):
         else:
             ctx.save_for_backward(xc, rstd.squeeze(-1), alpha)
         ctx.ln = ln
-        return z.to(x.dtype)
+        ctx.in_dtype = x.dtype
+        return z.to(out_dtype or x.dtype)
 
     @staticmethod
     def backward(ctx, gz):
@@ -181,20 +182,20 @@ class _NormRefFn(torch.autograd.Function):
         dbeta = None
         if ctx.ln and beta is not None and beta.requires_grad:
             dbeta = flat(g).sum(0).to(beta.dtype)
-        return dx.to(gz.dtype), dalpha, dbeta, None, None, None
+        return dx.to(ctx.in_dtype), dalpha, dbeta, None, None, None, None
 
 
 class NormRef(torch.nn.Module):
-    def __init__(self, p, ln: bool, eps=1e-6, fp32=True, device="cuda", gen=None, trainable=False):
+    def __init__(self, p, ln: bool, eps=1e-6, fp32=True, device="cuda", gen=None, trainable=False, out_dtype=None):
         super().__init__()
-        self.ln, self.eps, self.fp32, self.p = ln, eps, fp32, p
+        self.ln, self.eps, self.fp32, self.p, self.out_dtype = ln, eps, fp32, p, out_dtype
         self.weight = torch.nn.Parameter((1 + 0.1 * torch.randn(p, generator=gen)).to(device),
                                          requires_grad=trainable)
         self.bias = (torch.nn.Parameter((0.1 * torch.randn(p, generator=gen)).to(device), requires_grad=trainable)
                      if ln else None)
 
     def forward(self, x):
-        return _NormRefFn.apply(x, self.weight, self.bias, self.eps, self.ln, self.fp32)
+        return _NormRefFn.apply(x, self.weight, self.bias, self.eps, self.ln, self.fp32, self.out_dtype)
 
 
 class Attention(torch.nn.Module):
@@ -219,19 +220,23 @@ class SwiGLURef(torch.nn.Module):
 class Block(torch.nn.Module):
     def __init__(self, arch: str, c: int, hidden: int, heads: int, tuning: str = "full", rank: int = 4,
                  eps: float = 1e-6, dtype=torch.bfloat16, device="cuda", seed: int = 0, norm_fp32: bool = True,
-                 lora_init_b: float = 0.0):
+                 lora_init_b: float = 0.0, residual_fp32: bool = False):
         super().__init__()
         if arch not in ("vit", "llama"):
             raise ValueError("arch must be 'vit' or 'llama'")
         g = torch.Generator(device="cpu").manual_seed(seed)
         self.arch, self.c, self.hidden, self.tuning, self.eps = arch, c, hidden, tuning, eps
+        # residual_fp32: the AMP layout -- fp32 residual stream, 16-bit linears; the
+        # norms read fp32 and emit the linears' dtype (ours: msln/msrms_*_mixed)
+        self.residual_fp32, self.dtype = residual_fp32, dtype
+        nout = dtype if residual_fp32 else None
         ln, bias = arch == "vit", arch == "vit"
         self.modes = linear_modes(arch, tuning)
         mk = lambda name, i, o: Linear(i, o, bias, self.modes[name], rank, dtype, device, g, lora_init_b)
-        self.norm1 = NormRef(c, ln, eps, norm_fp32, device, g)
+        self.norm1 = NormRef(c, ln, eps, norm_fp32, device, g, out_dtype=nout)
         self.q, self.k, self.v = mk("q", c, c), mk("k", c, c), mk("v", c, c)
         self.attn = Attention(heads, causal=arch == "llama")
-        self.norm2 = NormRef(c, ln, eps, norm_fp32, device, g)
+        self.norm2 = NormRef(c, ln, eps, norm_fp32, device, g, out_dtype=nout)
         if arch == "vit":
             self.proj = mk("proj", c, c)
             self.fc1, self.fc2 = mk("fc1", c, hidden), mk("fc2", hidden, c)
@@ -256,7 +261,8 @@ class Block(torch.nn.Module):
             for nm, cons in ((m.norm1, [m.q, m.k, m.v]), (m.norm2, cons2)):
                 fold_affine(cons, nm.weight.detach(), None if nm.bias is None else nm.bias.detach())
             ms = modules.MSLayerNorm if m.arch == "vit" else modules.MSRMSNorm
-            m.norm1, m.norm2 = ms(m.c, m.eps), ms(m.c, m.eps)
+            od = m.dtype if m.residual_fp32 else None
+            m.norm1, m.norm2 = ms(m.c, m.eps, out_dtype=od), ms(m.c, m.eps, out_dtype=od)
             m.ms_norm = True
         if act:
             m.act = modules.ReGELU2() if m.arch == "vit" else modules.ReSwiGLU2()

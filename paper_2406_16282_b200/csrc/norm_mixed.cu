@@ -270,17 +270,25 @@ struct MixedPlan {
   int ngrp;
 };
 
-MixedPlan plan_mixed(int64_t cols, uintptr_t a, uintptr_t b, uintptr_t c) {
+#ifndef LMBP_MIX_FWD_V
+#define LMBP_MIX_FWD_V 4
+#endif
+#ifndef LMBP_MIX_BWD_V
+#define LMBP_MIX_BWD_V 4
+#endif
+// vmax: groups per thread of the CTA teams (the kernels are instantiated
+// for V = 4; a smaller vmax only widens the team).
+MixedPlan plan_mixed(int64_t cols, uintptr_t a, uintptr_t b, uintptr_t c, int vmax) {
   MixedPlan p{false, false, 0, 0, 0};
-  if (cols % 8 != 0 || (a | b | c) % 16 != 0 || cols > 8 * 512 * 4) return p;
+  if (cols % 8 != 0 || (a | b | c) % 16 != 0 || cols > 8 * 512 * vmax) return p;
   p.ngrp = (int)(cols / 8);
   p.vec = true;
   if (p.ngrp <= 32 * 4) {          // up to 1024 columns: a warp per row
     p.warp = true;
     p.V = (p.ngrp + 31) / 32;
-  } else {                         // a CTA of <= 512 threads per row, <= 4 groups per thread
+  } else {                         // a CTA of <= 512 threads per row, <= vmax groups per thread
     p.V = 4;
-    p.team = 32 * (int)((p.ngrp + 4 * 32 - 1) / (4 * 32));
+    p.team = 32 * (int)((p.ngrp + vmax * 32 - 1) / (vmax * 32));
   }
   return p;
 }
@@ -294,7 +302,7 @@ int occupancy_mixed(K kernel, int threads) {
 
 template <typename TO, int NORM>
 cudaError_t fwd_mixed_t(const float *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps, cudaStream_t s) {
-  const MixedPlan p = plan_mixed(cols, (uintptr_t)x, (uintptr_t)y, 0);
+  const MixedPlan p = plan_mixed(cols, (uintptr_t)x, (uintptr_t)y, 0, LMBP_MIX_FWD_V);
   const uint4 *xv = reinterpret_cast<const uint4 *>(x);
   uint4 *yv = reinterpret_cast<uint4 *>(y);
   if (p.vec && p.warp) {
@@ -323,7 +331,7 @@ cudaError_t fwd_mixed_t(const float *x, void *y, float *rstd, int64_t rows, int6
 template <typename TO, int NORM>
 cudaError_t bwd_mixed_t(const void *dy, const void *y, const float *rstd, float *dx, int64_t rows, int64_t cols,
                         cudaStream_t s) {
-  const MixedPlan p = plan_mixed(cols, (uintptr_t)dy, (uintptr_t)y, (uintptr_t)dx);
+  const MixedPlan p = plan_mixed(cols, (uintptr_t)dy, (uintptr_t)y, (uintptr_t)dx, LMBP_MIX_BWD_V);
   const uint4 *gv = reinterpret_cast<const uint4 *>(dy);
   const uint4 *yv = reinterpret_cast<const uint4 *>(y);
   uint4 *dv = reinterpret_cast<uint4 *>(dx);

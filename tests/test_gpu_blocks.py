@@ -193,3 +193,53 @@ def test_approx_block_trains(arch):
         o.backward(dy)
     assert 0 < rel(xs[1].grad, xs[0].grad) < 0.6
     assert saves_input("lora") and not saves_input("lora_fa")
+
+
+@pytest.mark.parametrize("tuning", ["full", "lora_qv", "lora_fa_all"])
+@pytest.mark.parametrize("arch", ["vit", "llama"])
+def test_amp_residual_fp32_block(arch, tuning):
+    """The AMP layout of Fig. 5 / 6: fp32 residual stream,
+    bf16 linears.  The reference norm saves the fp32 residual itself; ours is
+    the mixed MS norm (fp32 in, bf16 y out) keeping bf16 y + rstd.  Bytes per
+    module exact; the block's y bytewise = msln/msrms_fwd_mixed; its fp32 dx
+    within the fp32 norm-backward bound against the oracle on the delivered
+    bf16 gradient."""
+    s = SHAPES[arch]
+    exact = Block(arch, s["c"], s["hidden"], s["heads"], tuning=tuning, device=DEV, residual_fp32=True,
+                  lora_init_b=0.02)
+    ours = exact.to_ours()
+    b, n = 2, 64
+    R, c = b * n, exact.c
+    x = synth.norm_input(R, c, "f32").to(DEV).view(b, n, c).requires_grad_(True)
+    _, pe = activation_bytes(exact, x, by_module=True)
+    _, po = activation_bytes(ours, x, by_module=True)
+    stats = 8 * R if arch == "vit" else 4 * R
+    for name in ("norm1", "norm2"):
+        assert pe[name] == 4 * R * c + stats                   # the fp32 residual itself + statistics
+        assert po[name] == 2 * R * c + 4 * R                   # bf16 y + rstd
+    # internals: forward bytes and backward bound
+    rec, hs, pack = _capture(ours)
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = ours(x)
+    assert out.dtype == torch.float32
+    out.backward(synth.grad_input(R, c, "f32").to(DEV).view_as(out))
+    torch.cuda.synchronize()
+    for h in hs:
+        h.remove()
+    nf = P.msln_fwd_mixed if arch == "vit" else P.msrms_fwd_mixed
+    ob = oracle.msln_bwd if arch == "vit" else oracle.msrms_bwd
+    for name in ("norm1", "norm2"):
+        (xin,), y = rec[name]
+        assert xin.dtype == torch.float32 and y.dtype == torch.bfloat16
+        y_ref, r_ref = nf(xin.detach().contiguous(), ours.eps)
+        assert st(y).tobytes() == st(y_ref).tobytes(), name
+        (gin,), (gout,) = rec[name + "_bwd"]
+        g64 = dec(gout.detach().reshape(-1, c).cpu(), "bf16")
+        y64 = dec(y.detach().reshape(-1, c).cpu(), "bf16")
+        r64 = r_ref.reshape(-1).cpu().numpy().astype(np.float64)
+        ref = ob(g64, y64, r64)
+        m1 = np.abs(g64.mean(1, keepdims=True)) if arch == "vit" else 0.0
+        scale = r64[:, None] * (np.abs(g64) + m1 + np.abs(y64) * np.abs(g64 * y64).mean(1, keepdims=True))
+        got = gin.detach().reshape(-1, c).cpu().double().numpy()
+        assert gin.dtype == torch.float32
+        assert not (np.abs(got - ref) > 4e-5 * scale + 2.0 ** -126).any(), name

@@ -75,6 +75,8 @@ def main():
     xn = synth.norm_input(R, H, dt, device=dev)
     gn = synth.grad_input(R, H, dt, device=dev)
     yn, dxn = torch.empty_like(xn), torch.empty_like(gn)
+    xn32 = xn.float()                                 # fp32 residual stream for the mixed norms
+    dxn32 = torch.empty_like(xn32)
     rstd = torch.empty(R, dtype=torch.float32, device=dev)
     flush = torch.ones((2 * torch.cuda.get_device_properties(dev).L2_cache_size) // 4, device=dev)
     sink = torch.zeros((), device=dev)
@@ -87,6 +89,7 @@ def main():
               "step2_fwd": 2 * b * n + (n + 3) // 4, "step4_fwd": 2 * b * n + (n + 1) // 2,
               "step4_bwd": 2 * b * n + (n + 1) // 2, "step3_fwd": 2 * b * n + (3 * n + 7) // 8,
               "step3_bwd": 2 * b * n + (3 * n + 7) // 8,
+              "mnorm_fwd": (4 * H + b * H + 4) * R, "mnorm_bwd": (2 * b * H + 4 + 4 * H) * R,
               "swiglu_fwd": 4 * b * n + (n + 3) // 4, "swiglu_bwd": 5 * b * n + (n + 3) // 4}
     act = "regelu2" if cfg["act"] == "gelu" else "resilu2"
     nrm = "msln" if cfg["norm"] == "ln" else "msrms"
@@ -107,6 +110,12 @@ def main():
                                                    codes.data_ptr(), R, F, DT[dt], sp)
         calls["step4_fwd"] = lambda: L.stepact_fwd(ak, 4, ctypes.addressof(thr4), x.data_ptr(), y.data_ptr(),
                                                    codes4.data_ptr(), R, F, DT[dt], sp)
+        mk = 0 if cfg["norm"] == "ln" else 1
+        mfwd = getattr(L, nrm + "_fwd_mixed", None)
+        mbwd = getattr(L, nrm + "_bwd_mixed", None)
+        calls["mnorm_fwd"] = lambda: mfwd(xn32.data_ptr(), yn.data_ptr(), rstd.data_ptr(), R, H, 1e-6, DT[dt], sp)
+        calls["mnorm_bwd"] = lambda: mbwd(gn.data_ptr(), yn.data_ptr(), rstd.data_ptr(), dxn32.data_ptr(), R, H,
+                                          DT[dt], sp)
         calls["step3_fwd"] = lambda: L.stepact_fwd(ak, 3, ctypes.addressof(thr3), x.data_ptr(), y.data_ptr(),
                                                    codes3.data_ptr(), R, F, DT[dt], sp)
         calls["step3_bwd"] = lambda: L.stepact_bwd(3, ctypes.addressof(lv3), dy.data_ptr(), codes3.data_ptr(),
