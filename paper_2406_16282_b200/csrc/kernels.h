@@ -22,6 +22,9 @@ cudaError_t norm_fwd_mixed(int kind, int dtype, const float *x, void *y, float *
                            float eps, cudaStream_t s);
 cudaError_t norm_bwd_mixed(int kind, int dtype, const void *dy, const void *y, const float *rstd, float *dx,
                            int64_t rows, int64_t cols, cudaStream_t s);
+// the same on norm.cu's row pipeline; cudaErrorNotSupported when the row does not fit it
+cudaError_t norm_bwd_mixed_rows(int kind, int dtype, const void *dy, const void *y, const float *rstd, float *dx,
+                                int64_t rows, int64_t cols, cudaStream_t s);
 
 struct StepTable;  // common.cuh
 cudaError_t stepact_fwd(int act, int dtype, const StepTable &t, const void *x, void *y, uint8_t *codes, int64_t n,

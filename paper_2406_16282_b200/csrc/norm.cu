@@ -370,7 +370,9 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
 #ifndef LMBP_ROW_UNIT
 #define LMBP_ROW_UNIT 1
 #endif
-template <typename T, int NORM, bool kFwd, int V>
+// kF32Out (backward only): dx is written as fp32 (the mixed-precision
+// backward of norm_mixed.cu: 16-bit dy, y -> fp32 residual gradient).
+template <typename T, int NORM, bool kFwd, int V, bool kF32Out = false>
 __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 *b, const float *rstd_in, uint4 *out,
                                                     float *rstd_out, int64_t rows, int nvec, int cols, float eps,
                                                     int stages) {
@@ -554,7 +556,13 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
             const float c = NORM == kNormLN ? __fsub_rn(g[e], m1) : g[e];
             g[e] = __fmul_rn(r, fmaf(-h[e], m2, c));
           }
-          st_stream(orow + vi, Vec<T>::pack(g));
+          if constexpr (kF32Out) {
+            uint4 *o32 = out + row * (int64_t)nvec * 2;
+            st_stream(o32 + 2 * vi, Vec<float>::pack(g));
+            st_stream(o32 + 2 * vi + 1, Vec<float>::pack(g + 4));
+          } else {
+            st_stream(orow + vi, Vec<T>::pack(g));
+          }
         }
       }
     }
@@ -602,11 +610,11 @@ static RowTmaPlan plan_row_tma(int64_t nvec, bool fwd) {
   return p;
 }
 
-template <typename T, int NORM, bool kFwd, int V>
+template <typename T, int NORM, bool kFwd, int V, bool kF32Out = false>
 static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const void *b, const float *rstd_in,
                                     void *out, float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps,
                                     cudaStream_t s) {
-  auto kern = norm_row_tma<T, NORM, kFwd, V>;
+  auto kern = norm_row_tma<T, NORM, kFwd, V, kF32Out>;
   static std::atomic<unsigned long long> smem_set{0};
   const cudaError_t e = ensure_dyn_smem(kern, 227 * 1024, smem_set);
   if (e != cudaSuccess) return e;
@@ -619,14 +627,14 @@ static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const v
   return cudaGetLastError();
 }
 
-template <typename T, int NORM, bool kFwd>
+template <typename T, int NORM, bool kFwd, bool kF32Out = false>
 static cudaError_t launch_row_tma(const RowTmaPlan &rp, const void *a, const void *b, const float *rstd_in, void *out,
                                   float *rstd_out, int64_t rows, int nvec, int64_t cols, float eps, cudaStream_t s) {
   switch (rp.V) {
-    case 1: return launch_row_tma_v<T, NORM, kFwd, 1>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 2: return launch_row_tma_v<T, NORM, kFwd, 2>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    case 3: return launch_row_tma_v<T, NORM, kFwd, 3>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
-    default: return launch_row_tma_v<T, NORM, kFwd, 4>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 1: return launch_row_tma_v<T, NORM, kFwd, 1, kF32Out>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 2: return launch_row_tma_v<T, NORM, kFwd, 2, kF32Out>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    case 3: return launch_row_tma_v<T, NORM, kFwd, 3, kF32Out>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
+    default: return launch_row_tma_v<T, NORM, kFwd, 4, kF32Out>(rp, a, b, rstd_in, out, rstd_out, rows, nvec, cols, eps, s);
   }
 }
 
@@ -938,6 +946,23 @@ static cudaError_t norm_bwd_t(const void *dy, const void *y, const float *rstd, 
   }
 #undef LMBP_BWD_CASE
   return cudaGetLastError();
+}
+
+// Mixed-precision backward on the row pipeline (norm_mixed.cu): 16-bit dy, y
+// (dtype 1 / 2) -> fp32 dx, for rows the ring holds (>= 256 vectors, as the
+// same-type backward); cudaErrorNotSupported otherwise (the caller falls back).
+cudaError_t norm_bwd_mixed_rows(int kind, int dtype, const void *dy, const void *y, const float *rstd, float *dx,
+                                int64_t rows, int64_t cols, cudaStream_t s) {
+  if (cols % 8 != 0 || ((uintptr_t)dy | (uintptr_t)y | (uintptr_t)dx) % 16 != 0 || rows <= 0)
+    return cudaErrorNotSupported;
+  const int64_t nvec = cols / 8;
+  const RowTmaPlan rp = plan_row_tma(nvec, false);
+  if (!rp.ok) return cudaErrorNotSupported;
+  if (kind == kNormLN)
+    return dtype == 1 ? launch_row_tma<__nv_bfloat16, kNormLN, false, true>(rp, dy, y, rstd, dx, nullptr, rows, (int)nvec, cols, 0.0f, s)
+                      : launch_row_tma<__half, kNormLN, false, true>(rp, dy, y, rstd, dx, nullptr, rows, (int)nvec, cols, 0.0f, s);
+  return dtype == 1 ? launch_row_tma<__nv_bfloat16, kNormRMS, false, true>(rp, dy, y, rstd, dx, nullptr, rows, (int)nvec, cols, 0.0f, s)
+                    : launch_row_tma<__half, kNormRMS, false, true>(rp, dy, y, rstd, dx, nullptr, rows, (int)nvec, cols, 0.0f, s);
 }
 
 cudaError_t norm_fwd(int kind, int dtype, const void *x, void *y, float *rstd, int64_t rows, int64_t cols, float eps,

@@ -372,6 +372,14 @@ cudaError_t norm_fwd_mixed(int kind, int dtype, const float *x, void *y, float *
 
 cudaError_t norm_bwd_mixed(int kind, int dtype, const void *dy, const void *y, const float *rstd, float *dx,
                            int64_t rows, int64_t cols, cudaStream_t s) {
+#ifndef LMBP_MIX_NO_ROWS
+  // rows of >= 256 16-byte vectors of dy (H >= 2048): the TMA row pipeline
+  // of the same-type backward, writing fp32 (C4 49.2 -> see DESIGN 5.9)
+  if (cols >= 2048) {
+    const cudaError_t e = norm_bwd_mixed_rows(kind, dtype, dy, y, rstd, dx, rows, cols, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
+#endif
   if (kind == kNormLN)
     return dtype == 1 ? bwd_mixed_t<__nv_bfloat16, kNormLN>(dy, y, rstd, dx, rows, cols, s)
                       : bwd_mixed_t<__half, kNormLN>(dy, y, rstd, dx, rows, cols, s);
