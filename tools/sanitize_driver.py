@@ -35,6 +35,10 @@ for dt in ("f32", "bf16", "f16"):
         for fwd, bwd in ((P.msln_fwd, P.msln_bwd), (P.msrms_fwd, P.msrms_bwd)):
             yn, r = fwd(xn, 1e-6)
             bwd(gn, yn, r)
+        if dt != "f32":                                  # mixed: fp32 residual in, 16-bit y out
+            for fwd, bwd in ((P.msln_fwd_mixed, P.msln_bwd_mixed), (P.msrms_fwd_mixed, P.msrms_bwd_mixed)):
+                ym, rm = fwd(xn.float(), 1e-6, xn.dtype)
+                bwd(gn, ym, rm)
 # coefficient fitter (fp64): objective for k = 1..3, a short anneal + refine
 for act in ("gelu", "silu"):
     for k in (1, 2, 3):
