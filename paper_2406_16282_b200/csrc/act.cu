@@ -378,7 +378,19 @@ extern "C" __attribute__((visibility("default"))) int lmbp_trace_act(unsigned lo
   if (reset) {
     const unsigned int z = 0;
     if (cudaMemcpyToSymbol(lmbp::lmbp_trace_n, &z, sizeof(z)) != cudaSuccess) return -1;
+    if (cudaMemcpyToSymbol(lmbp::lmbp_trace_un, &z, sizeof(z)) != cudaSuccess) return -1;
   }
+  return m;
+}
+
+// Diagnostic build only: the (unit, time) pairs of the CLC claims.
+extern "C" __attribute__((visibility("default"))) int lmbp_trace_units_act(unsigned long long *host, int max_pairs) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, lmbp::lmbp_trace_un, sizeof(n)) != cudaSuccess) return -1;
+  const int m = (int)(n < (unsigned)max_pairs ? n : (unsigned)max_pairs);
+  if (m > 0 && cudaMemcpyFromSymbol(host, lmbp::lmbp_trace_units, (size_t)m * 2 * sizeof(unsigned long long)) !=
+                   cudaSuccess)
+    return -1;
   return m;
 }
 #endif

@@ -33,6 +33,7 @@ struct EwParams {
   uint8_t *codes_out;        // packed codes written by forward ops
   int64_t nvec;              // whole 16-byte vectors
   int64_t n;                 // elements
+  int64_t end_zone;          // set by launch_ew: tiles >= end_zone keep at most LMBP_EW_END_DEPTH in flight
 };
 
 // An Op may extend the parameters (`using Params = ...;`, derived from
@@ -130,6 +131,14 @@ __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
 #ifndef LMBP_EW_UNIT
 #define LMBP_EW_UNIT 1
 #endif
+// End-zone depth (tools/sweep.py knob; 0 = off): the last LMBP_EW_END_MULT x
+// (resident CTAs) tiles run with at most LMBP_EW_END_DEPTH stages queued.
+#ifndef LMBP_EW_END_DEPTH
+#define LMBP_EW_END_DEPTH 0
+#endif
+#ifndef LMBP_EW_END_MULT
+#define LMBP_EW_END_MULT 2
+#endif
 
 // Optional per-CTA lookup table in shared memory: an Op with
 // `static constexpr int kLut` and `static float lut_entry(const Params &, int)`
@@ -151,6 +160,8 @@ __device__ __forceinline__ uint32_t apply_op(const uint4 (&v)[NIN], uint32_t c, 
 // globaltimer nanoseconds.  Each translation unit has its own buffer.
 static __device__ unsigned long long lmbp_trace_buf[8192 * 5];
 static __device__ unsigned int lmbp_trace_n;
+static __device__ unsigned long long lmbp_trace_units[65536 * 2];  // (unit claimed via CLC, time)
+static __device__ unsigned int lmbp_trace_un;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -241,6 +252,15 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         for (int64_t t = unit * LMBP_EW_UNIT; t < t_end; ++t, ++k) {
           const int s = k % S;
           mbar_wait(&empty[s], ((uint32_t)(k / S) & 1u) ^ 1u);
+#if LMBP_EW_END_DEPTH > 0
+          // End zone: keep at most LMBP_EW_END_DEPTH tiles queued, so when the
+          // work runs out no CTA still holds a deep ring to drain at its own
+          // (possibly slower) rate; the faster CTAs take the last tiles.
+          if (t >= p.end_zone && k >= LMBP_EW_END_DEPTH && LMBP_EW_END_DEPTH < S) {
+            const int j = k - LMBP_EW_END_DEPTH;
+            mbar_wait(&empty[j % S], (uint32_t)(j / S) & 1u);
+          }
+#endif
           slot[s] = t;
           if (t == ntiles) {             // leftover pseudo-tile: nothing to load
             mbar_arrive(&full[s]);
@@ -257,6 +277,15 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         mbar_wait(clc_bar, clc_phase);
         clc_phase ^= 1u;
         const int next = clc_query(clc_resp);
+#ifdef LMBP_TRACE
+        if (next >= 0) {
+          const unsigned int q = atomicAdd(&lmbp_trace_un, 1u);
+          if (q < 65536) {
+            lmbp_trace_units[2 * q] = (unsigned long long)next;
+            lmbp_trace_units[2 * q + 1] = gtimer();
+          }
+        }
+#endif
         more = next >= 0;
         unit = next;
       }

@@ -51,6 +51,7 @@ def main():
         for name, path in libs.items():
             L = ctypes.CDLL(path)
             L.lmbp_trace_act.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+            L.lmbp_trace_units_act.argtypes = [ctypes.c_void_p, ctypes.c_int]
             f = getattr(L, act + "_fwd")
             b = getattr(L, act + "_bwd")
             for fn in (f, b):
@@ -68,6 +69,8 @@ def main():
                     assert fn() == 0
                     e1.record(st)
                     torch.cuda.synchronize()
+                    ub = (ctypes.c_ulonglong * (65536 * 2))()
+                    nu = L.lmbp_trace_units_act(ctypes.addressof(ub), 65536)
                     n = L.lmbp_trace_act(ctypes.addressof(buf), 8192, 1)
                     r = np.array(buf[:5 * n], dtype=np.float64).reshape(n, 5)
                     t0 = r[:, 1].min()
@@ -81,7 +84,17 @@ def main():
                                 "exit_p50_us": float(np.median(ext)) / 1e3,
                                 "tiles_min": int(tiles.min()), "tiles_max": int(tiles.max()),
                                 "tiles_total": int(tiles.sum())})
-                med = {kk: round(float(np.median([q[kk] for q in res[2:]])), 3) for kk in res[0]}
+                    if nu > 0:
+                        u = np.array(ub[:2 * nu], dtype=np.float64).reshape(nu, 2)
+                        u = u[np.argsort(u[:, 1])]
+                        # claim order vs unit index: rank correlation and the index range of the last 5 %
+                        order = np.argsort(np.argsort(u[:, 0]))
+                        rc = float(np.corrcoef(order, np.arange(nu))[0, 1])
+                        tail = u[int(0.95 * nu):, 0]
+                        res[-1].update({"claims": int(nu), "claim_order_corr": round(rc, 4),
+                                        "last5pct_unit_min": int(tail.min()), "last5pct_unit_max": int(tail.max()),
+                                        "units_total": int(u[:, 0].max())})
+                med = {kk: round(float(np.median([q[kk] for q in res[2:] if kk in q])), 3) for kk in res[-1]}
                 print(json.dumps({"variant": name, "config": cname, "kernel": k, **med}), flush=True)
 
 
