@@ -33,7 +33,6 @@ struct EwParams {
   uint8_t *codes_out;        // packed codes written by forward ops
   int64_t nvec;              // whole 16-byte vectors
   int64_t n;                 // elements
-  int64_t end_zone;          // set by launch_ew: tiles >= end_zone keep at most LMBP_EW_END_DEPTH in flight
 };
 
 // An Op may extend the parameters (`using Params = ...;`, derived from
@@ -130,14 +129,6 @@ __device__ __forceinline__ uint32_t code_word(const uint8_t *base, int64_t i) {
 // (written before the stage's mbarrier arrive, read after its wait); -1 ends.
 #ifndef LMBP_EW_UNIT
 #define LMBP_EW_UNIT 1
-#endif
-// End-zone depth (tools/sweep.py knob; 0 = off): the last LMBP_EW_END_MULT x
-// (resident CTAs) tiles run with at most LMBP_EW_END_DEPTH stages queued.
-#ifndef LMBP_EW_END_DEPTH
-#define LMBP_EW_END_DEPTH 0
-#endif
-#ifndef LMBP_EW_END_MULT
-#define LMBP_EW_END_MULT 2
 #endif
 
 // Optional per-CTA lookup table in shared memory: an Op with
@@ -252,15 +243,6 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         for (int64_t t = unit * LMBP_EW_UNIT; t < t_end; ++t, ++k) {
           const int s = k % S;
           mbar_wait(&empty[s], ((uint32_t)(k / S) & 1u) ^ 1u);
-#if LMBP_EW_END_DEPTH > 0
-          // End zone: keep at most LMBP_EW_END_DEPTH tiles queued, so when the
-          // work runs out no CTA still holds a deep ring to drain at its own
-          // (possibly slower) rate; the faster CTAs take the last tiles.
-          if (t >= p.end_zone && k >= LMBP_EW_END_DEPTH && LMBP_EW_END_DEPTH < S) {
-            const int j = k - LMBP_EW_END_DEPTH;
-            mbar_wait(&empty[j % S], (uint32_t)(j / S) & 1u);
-          }
-#endif
           slot[s] = t;
           if (t == ntiles) {             // leftover pseudo-tile: nothing to load
             mbar_arrive(&full[s]);
@@ -380,12 +362,13 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
 
 // Launch one CTA per work unit; resident CTAs steal the rest through CLC.
 template <class Op>
-cudaError_t launch_ew(const typename ParamsOf<Op>::type &p, cudaStream_t stream) {
+cudaError_t launch_ew(const typename ParamsOf<Op>::type &p_in, cudaStream_t stream) {
   using Sh = EwShape<Op>;
   auto kern = ew_tma<Op>;
   static std::atomic<unsigned long long> smem_set{0};
   const cudaError_t e = ensure_dyn_smem(kern, Sh::kSmem, smem_set);
   if (e != cudaSuccess) return e;
+  typename ParamsOf<Op>::type p = p_in;
   const int64_t items = p.nvec / Sh::kTile + 1;
   const int64_t units = (items + LMBP_EW_UNIT - 1) / LMBP_EW_UNIT;
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
