@@ -88,7 +88,7 @@ def build_variant(name: str, defines, sources=None) -> str:
     import hashlib
     tag = hashlib.sha1("\n".join(sorted(defines)).encode()).hexdigest()[:8]
     name = f"{name}-{tag}"                     # same name, different -D set: a different build
-    vdir = os.path.join(HERE, "_variants", name)
+    vdir = os.path.join(HERE, "_variant_obj", name)
     os.makedirs(vdir, exist_ok=True)
     ensure_lut()
     srcs = SOURCES if sources is None else list(sources)
@@ -96,9 +96,12 @@ def build_variant(name: str, defines, sources=None) -> str:
         objs = list(ex.map(lambda s: _compile(s, vdir, defines), srcs))
     # sources left out are linked from the product build (knob-independent, e.g. fit.cu)
     objs += [_compile(s) for s in SOURCES if s not in srcs]
+    os.makedirs(os.path.join(HERE, "_variants"), exist_ok=True)
     out = os.path.join(HERE, "_variants", f"liblmbp_{name}.so")
     if _stale(out, objs) or not os.path.exists(out):
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
+    import shutil
+    shutil.rmtree(vdir, ignore_errors=True)          # objects are only a cache; keep the snapshot small
     return out
 
 

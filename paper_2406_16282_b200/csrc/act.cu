@@ -146,6 +146,9 @@ __device__ __forceinline__ uint32_t act_vec_op(const uint4 &v, uint32_t c_in, ui
     if constexpr (kVec == 4) c = codes_vec_f32<A>(f);
     else c = codes_vec_16<T, A>(v);
 #ifndef LMBP_DIAG_NO_MATH  // diagnostic build knob (tools/sweep.py): time the pipeline without the math
+#ifdef LMBP_DIAG_SKIP_LO     // diagnostic: no math for vectors [LO, HI) only (start / end transients)
+    if (!(i >= (int64_t)LMBP_DIAG_SKIP_LO && i < (int64_t)LMBP_DIAG_SKIP_HI))
+#endif
 #pragma unroll
     for (int k = 0; k < kVec; k += 2) {
       const float2 r = act2_f<A, kPrecise>(make_float2(f[k], f[k + 1]));

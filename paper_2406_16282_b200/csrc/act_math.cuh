@@ -3,10 +3,12 @@
 //   forward : y = GELU(x) or SiLU(x), unchanged;
 //             code = #{i : x > c_i}, 2 bits per element.
 //   backward: dx = dy * s[code], s = (0, a1, a1 + a2, 1).
-// GELU is evaluated branch-free as max(x,0) - |x| e^{-x^2/2} G(|x|),
+// GELU is evaluated branch-free as max(x,-0) - |x| e^{-x^2/2} G(|x|),
 // G(u) = Phi(-u) e^{u^2/2} ~= t P6(t), t = 1/(1 + k u); SiLU as
-// max(x,0) - u e^{-u} / (1 + e^{-u}) with e^{-u} = (e^{-u/2})^2.  fp32 outputs
-// add an exact split of the exponent argument ("precise").
+// max(x,-0) - u e^{-u} / (1 + e^{-u}) with e^{-u} = (e^{-u/2})^2.  fp32 outputs
+// add an exact split of the exponent argument ("precise").  The relu term is
+// max(x, -0), so a negative x whose product underflows returns -0, the sign
+// of the exact value (x Phi(x), x sigma(x) < 0), and x = +-0 returns +-0.
 #pragma once
 #include <type_traits>
 
@@ -83,7 +85,7 @@ __device__ __forceinline__ float gelu_f(float x) {
   } else {
     e = ex2_approx(__fmul_rn(__fmul_rn(u, u), __uint_as_float(kExpKH)));
   }
-  return fmaf(-q, e, fmaxf(x, 0.0f));
+  return fmaf(-q, e, fmaxf(x, -0.0f));
 }
 
 // SiLU(x) = x sigma(x) = max(x,0) - u sigma(-u) = max(x,0) - u e^{-u} / (1 + e^{-u}).
@@ -96,7 +98,7 @@ __device__ __forceinline__ float silu_f(float x) {
   // path: ptxas fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2 regardless of the
   // rounding modifier, so the contract is written as the fused form on both).
   const float nq = __fmul_rn(__fmul_rn(-u, eh), s);
-  return fmaf(nq, eh, fmaxf(x, 0.0f));
+  return fmaf(nq, eh, fmaxf(x, -0.0f));
 }
 
 // Packed-pair versions on sm_100's f32x2 FMA pipe (FFMA2 / FMUL2): the same
@@ -124,7 +126,7 @@ __device__ __forceinline__ float2 gelu2_f(float2 x) {
     const float2 nq = __fmul2_rn(nu, __fmul2_rn(t, p));  // -u G(u), exact negation of q
     const float2 a = __fmul2_rn(__fmul2_rn(u, u), f2(__uint_as_float(kExpKH)));
     const float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-    return __ffma2_rn(nq, e, make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
+    return __ffma2_rn(nq, e, make_float2(fmaxf(x.x, -0.0f), fmaxf(x.y, -0.0f)));
   }
 }
 
@@ -135,11 +137,19 @@ __device__ __forceinline__ float2 silu2_f(float2 x) {
   } else {
     const float2 u = make_float2(fabsf(x.x), fabsf(x.y));
     const float2 a = __fmul2_rn(u, f2(__uint_as_float(kExpKH)));
+#ifdef LMBP_DIAG_NO_EX2  // diagnostic build knobs: the MUFU ops replaced by FMUL (wrong values; timing only)
+    const float2 eh = __fmul2_rn(a, f2(0.25f));
+#else
     const float2 eh = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+#endif
     const float2 d = __ffma2_rn(eh, eh, f2(1.0f));
+#ifdef LMBP_DIAG_NO_RCP
+    const float2 s = __fmul2_rn(d, f2(0.75f));
+#else
     const float2 s = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+#endif
     const float2 nq = __fmul2_rn(__fmul2_rn(make_float2(-u.x, -u.y), eh), s);
-    return __ffma2_rn(nq, eh, make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)));
+    return __ffma2_rn(nq, eh, make_float2(fmaxf(x.x, -0.0f), fmaxf(x.y, -0.0f)));
   }
 }
 

@@ -33,9 +33,10 @@ FORMATS = {  # significant bits, min normal exponent, max finite
 def inputs(fmt: str) -> np.ndarray:
     """float64 values of all 65536 bit patterns (NaN for NaN patterns)."""
     b = np.arange(65536, dtype=np.uint32)
-    if fmt == "bf16":
-        return (b << 16).astype(np.uint32).view(np.float32).astype(np.float64)
-    return b.astype(np.uint16).view(np.float16).astype(np.float64)
+    with np.errstate(invalid="ignore"):   # the NaN patterns widen to NaN
+        if fmt == "bf16":
+            return (b << 16).astype(np.uint32).view(np.float32).astype(np.float64)
+        return b.astype(np.uint16).view(np.float16).astype(np.float64)
 
 
 def _gelu64(x: np.ndarray) -> np.ndarray:

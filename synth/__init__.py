@@ -151,3 +151,19 @@ def codes_input(n: int, *, device="cpu", base: int = BASE_SEED) -> torch.Tensor:
     if n % 4 and nbytes:
         b[-1] &= (1 << (2 * (n % 4))) - 1
     return b.to(device)
+
+
+def all_patterns16(dtype: str, *, finite_only: bool = False, cols: int = 256) -> torch.Tensor:
+    """Every bf16 / fp16 bit pattern once, in ascending pattern order, as a
+    [rows, cols] tensor (65 536 elements; NaN and +-inf included unless
+    finite_only, then the 256 (bf16) / 2 048 (fp16) all-ones-exponent
+    patterns are dropped).  The exhaustive 16-bit parity input."""
+    import numpy as np
+    assert dtype in ("bf16", "f16")
+    b = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    if finite_only:
+        shift, emask = (7, 0xFF) if dtype == "bf16" else (10, 0x1F)
+        b = b[((b >> shift) & emask) != emask]
+    t = torch.from_numpy(b.view(np.int16).copy())
+    t = t.view(torch.bfloat16) if dtype == "bf16" else t.view(torch.float16)
+    return t.reshape(-1, cols).contiguous()

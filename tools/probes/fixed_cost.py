@@ -1,0 +1,98 @@
+"""Fixed vs per-byte cost of the activation kernels across library variants
+(tools/sweep.py's variant syntax: name:DEF1,DEF2 or name:@path/to/lib.so):
+time act_fwd / act_bwd of each variant and a torch copy at several row counts
+of one width with the bench protocol (L2 flushed by a 2 x L2 read, CUDA
+events, median of --iters), fit t = a + bytes / r per (variant, kernel).
+Prints one JSON line per point and one per fit."""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2406_16282_b200 import build as B  # noqa: E402
+from sweep import load  # noqa: E402
+
+DT = {"f32": 0, "bf16": 1, "f16": 2}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--act", default="silu")
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--cols", type=int, default=11008)
+    ap.add_argument("--rows", default="1024,2048,4096,8192,16384")
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--kernels", default="fwd,bwd")
+    ap.add_argument("--variants", nargs="+", default=["base:"])
+    ap.add_argument("--build-only", action="store_true")
+    a = ap.parse_args()
+    libs = {}
+    for v in a.variants:
+        name, _, defs = v.partition(":")
+        libs[name] = (os.path.join(ROOT, defs[1:]) if defs.startswith("@") else
+                      B.build_variant(name, [d for d in defs.split(",") if d],
+                                      sources=[s for s in B.SOURCES if s != "fit.cu"]))
+    if a.build_only:
+        return
+    dev = torch.device("cuda")
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.ones(max(2 * l2, 256 << 20) // 4, device=dev)
+    sink = torch.zeros((), device=dev)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+    act = "regelu2" if a.act == "gelu" else "resilu2"
+    L = {k: load(p) for k, p in libs.items()}
+    pts = {}
+    for R in [int(r) for r in a.rows.split(",")]:
+        x = synth.act_input(R, a.cols, a.dtype, device=dev)
+        dy = synth.grad_input(R, a.cols, a.dtype, device=dev)
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        n, b = x.numel(), x.element_size()
+        codes = torch.empty((n + 3) // 4, dtype=torch.uint8, device=dev)
+        nb = 2 * b * n + (n + 3) // 4
+        fns = {("torch", "copy"): (lambda: (y.copy_(x), 0)[1], 2 * b * n)}
+        for name, lib in L.items():
+            f, bw = getattr(lib, act + "_fwd"), getattr(lib, act + "_bwd")
+            if "fwd" in a.kernels:
+                fns[(name, "fwd")] = (lambda f=f: f(x.data_ptr(), y.data_ptr(), codes.data_ptr(), R, a.cols,
+                                                    DT[a.dtype], sp), nb)
+            if "bwd" in a.kernels:
+                fns[(name, "bwd")] = (lambda bw=bw: bw(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), R, a.cols,
+                                                       DT[a.dtype], sp), nb)
+        for key, (fn, nbytes) in fns.items():
+            for _ in range(3):
+                assert fn() == 0
+            ev = []
+            for _ in range(a.iters):
+                sink.copy_(flush.sum())
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                fn()
+                e1.record(st)
+                ev.append((e0, e1))
+            torch.cuda.synchronize()
+            us = float(np.median([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev]))
+            pts.setdefault(key, []).append((nbytes, us))
+            print(json.dumps({"variant": key[0], "kernel": key[1], "rows": R, "cols": a.cols, "bytes": nbytes,
+                              "us": round(us, 2), "GB/s": round(nbytes / us / 1e3, 1)}), flush=True)
+        del x, dy, y, dx, codes
+        torch.cuda.empty_cache()
+    for key, v in pts.items():
+        Bv = np.array([p[0] for p in v], dtype=np.float64)
+        T = np.array([p[1] for p in v])
+        A = np.stack([np.ones_like(Bv), Bv], 1)
+        (c0, c1), *_ = np.linalg.lstsq(A, T, rcond=None)
+        print(json.dumps({"fit": key[1], "variant": key[0], "fixed_us": round(float(c0), 2),
+                          "GB/s_marginal": round(1e-3 / float(c1), 1)}))
+
+
+if __name__ == "__main__":
+    main()
