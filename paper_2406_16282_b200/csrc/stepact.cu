@@ -246,16 +246,15 @@ __device__ __forceinline__ uint32_t step_codes_vec(const uint4 &r, const float *
 // x > t <=> p > A(t); for p >= 0x8000, x falls with p and x > t <=> p < B(t),
 // with A(t) = -1, B(t) = bits(t) for t < 0 and A(t) = bits(t) & 0x7fff,
 // B(t) = 0 otherwise (t = RD_T(c), exact, reading R2); NaN patterns get 0.
-// A chunk of patterns is written a word (4 codes) at a time while no key
-// falls inside the word, else recounted pattern by pattern.
+// Each consumer thread writes 16-byte vectors of the table, their codes found
+// by binary search (a linear recount per 64-byte chunk, with boundary chunks
+// redone word by word, cost ~10 us more per launch at k = 4, and contiguous
+// per-thread runs walked monotonically cost more still -- strided 16-byte
+// stores -- profiles/r02/session4/fixed_cost_kbit*.jsonl).
 // ---------------------------------------------------------------------------
 template <typename T> struct Pat16;
 template <> struct Pat16<__nv_bfloat16> { static constexpr int kInf = 0x7F80; };
 template <> struct Pat16<__half> { static constexpr int kInf = 0x7C00; };
-
-#ifndef LMBP_CTAB_CHUNK
-#define LMBP_CTAB_CHUNK 64
-#endif
 
 template <typename T, int K>
 __device__ __forceinline__ void fill_code_table(uint8_t *ctab, const StepTable &tab, int tid, int nthr) {
@@ -268,52 +267,47 @@ __device__ __forceinline__ void fill_code_table(uint8_t *ctab, const StepTable &
     sB[tid] = negt ? tb : 0;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-  auto recount = [&](int q) -> int {
-    int c = 0;
-    if (q < 0x8000) {
+#ifndef LMBP_DIAG_NO_FILL  // diagnostic (timing only): leave the table unwritten
+  // code(q) = #{j : sA[j] < q} (q < 0x8000) or #{j : sB[j] > q} (q >= 0x8000).
+  // Both predicates hold on a prefix of j (sA is non-decreasing, sB
+  // non-increasing: the thresholds are sorted), so the count is a binary
+  // search for the prefix length: K dependent shared-memory loads.
+  auto code_of = [&](int q) -> uint32_t {
+    int lo = 0;
 #pragma unroll
-      for (int j = 0; j < M; ++j) c += sA[j] < q;
+    for (int step = 1 << (K - 1); step; step >>= 1) {
+      const int j = lo + step - 1;
+      if (j < M && (q < 0x8000 ? sA[j] < q : sB[j] > q)) lo += step;
+    }
+    return (uint32_t)lo;
+  };
+  // One 16-byte vector of the table (16 patterns, never straddling 0x8000)
+  // per step, lane-consecutive (conflict-free stores); the code is monotone
+  // within a half, so equal codes at both ends make a constant vector.  Only
+  // the ~2^(K+1) vectors holding a threshold (or the NaN boundary) are filled
+  // pattern by pattern.  Two vectors per iteration: four independent searches
+  // in flight (C4 k = 4: 75.8 -> 69.7 us, k = 3: 71.7 -> 69.8 us).
+#pragma unroll 2
+  for (int v = tid; v < 65536 / 16; v += nthr) {
+    const int p0 = 16 * v;
+    const int nan_lo = (p0 >= 0x8000 ? (0x8000 | Pat16<T>::kInf) : Pat16<T>::kInf) + 1;
+    const uint32_t c0 = code_of(p0), c1 = code_of(p0 + 15);
+    uint32_t w[4];
+    if (c0 == c1 && p0 + 15 < nan_lo) {
+      w[0] = w[1] = w[2] = w[3] = c0 * 0x01010101u;
     } else {
 #pragma unroll
-      for (int j = 0; j < M; ++j) c += sB[j] > q;
-    }
-    return c;
-  };
-  constexpr int CH = LMBP_CTAB_CHUNK;
-  static_assert(CH % 16 == 0, "chunks are written as 16-byte vectors");
-  for (int ch = tid; ch < 65536 / CH; ch += nthr) {
-    const int p0 = ch * CH;
-    const bool neg = p0 >= 0x8000;
-    const int nan_lo = (neg ? (0x8000 | Pat16<T>::kInf) : Pat16<T>::kInf) + 1;  // first NaN pattern of the half
-    int code = recount(p0);
-    // the code is monotone within a half: equal codes at both ends = constant chunk
-    if (p0 + CH - 1 < nan_lo && recount(p0 + CH - 1) == code) {
-      const uint32_t w = (uint32_t)code * 0x01010101u;
-#pragma unroll
-      for (int q = 0; q < CH; q += 16) *reinterpret_cast<uint4 *>(ctab + p0 + q) = make_uint4(w, w, w, w);
-      continue;
-    }
-    for (int e = 0; e < CH; e += 4) {  // a key (or the NaN boundary) falls inside: word by word
-      const int pe = p0 + e;
-      bool fast = pe + 3 < nan_lo;
-      if (!neg) fast = fast && (code == M || pe + 4 <= sA[code]);
-      else fast = fast && (code == 0 || pe + 4 < sB[code - 1]);
-      uint32_t word;
-      if (fast) {
-        word = (uint32_t)code * 0x01010101u;
-      } else {
-        word = 0;
-#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        w[e] = 0;
         for (int q = 0; q < 4; ++q) {
-          const int pq = pe + q;
-          const uint32_t c = pq >= nan_lo ? 0u : (uint32_t)recount(pq);
-          word |= c << (8 * q);
+          const int pq = p0 + 4 * e + q;
+          w[e] |= (pq >= nan_lo ? 0u : code_of(pq)) << (8 * q);
         }
-        code = recount(pe + 4 < 65536 ? pe + 4 : pe);
       }
-      *reinterpret_cast<uint32_t *>(ctab + pe) = word;
     }
+    *reinterpret_cast<uint4 *>(ctab + p0) = make_uint4(w[0], w[1], w[2], w[3]);
   }
+#endif
 }
 
 // Codes of one 16-byte vector (8 16-bit elements) from the code table.

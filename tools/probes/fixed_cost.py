@@ -21,6 +21,8 @@ from paper_2406_16282_b200 import build as B  # noqa: E402
 from sweep import load  # noqa: E402
 
 DT = {"f32": 0, "bf16": 1, "f16": 2}
+THR4 = (ctypes.c_double * 15)(*[-3.0 + 0.4 * i for i in range(15)])   # as tools/sweep.py
+THR3 = (ctypes.c_double * 7)(*[-3.0 + 1.0 * i for i in range(7)])
 
 
 def main():
@@ -58,12 +60,23 @@ def main():
         n, b = x.numel(), x.element_size()
         codes = torch.empty((n + 3) // 4, dtype=torch.uint8, device=dev)
         nb = 2 * b * n + (n + 3) // 4
+        codes4 = torch.empty((n + 1) // 2, dtype=torch.uint8, device=dev)
+        codes3 = torch.empty((3 * n + 7) // 8, dtype=torch.uint8, device=dev)
+        ak = 0 if a.act == "gelu" else 1
         fns = {("torch", "copy"): (lambda: (y.copy_(x), 0)[1], 2 * b * n)}
         for name, lib in L.items():
             f, bw = getattr(lib, act + "_fwd"), getattr(lib, act + "_bwd")
             if "fwd" in a.kernels:
                 fns[(name, "fwd")] = (lambda f=f: f(x.data_ptr(), y.data_ptr(), codes.data_ptr(), R, a.cols,
                                                     DT[a.dtype], sp), nb)
+            if "step4" in a.kernels:
+                fns[(name, "step4")] = (lambda lib=lib: lib.stepact_fwd(ak, 4, ctypes.addressof(THR4), x.data_ptr(),
+                                                                      y.data_ptr(), codes4.data_ptr(), R, a.cols,
+                                                                      DT[a.dtype], sp), 2 * b * n + (n + 1) // 2)
+            if "step3" in a.kernels:
+                fns[(name, "step3")] = (lambda lib=lib: lib.stepact_fwd(ak, 3, ctypes.addressof(THR3), x.data_ptr(),
+                                                                      y.data_ptr(), codes3.data_ptr(), R, a.cols,
+                                                                      DT[a.dtype], sp), 2 * b * n + (3 * n + 7) // 8)
             if "bwd" in a.kernels:
                 fns[(name, "bwd")] = (lambda bw=bw: bw(dy.data_ptr(), codes.data_ptr(), dx.data_ptr(), R, a.cols,
                                                        DT[a.dtype], sp), nb)
