@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--kernels", default="fwd,bwd")
     ap.add_argument("--variants", nargs="+", default=["base:"])
     ap.add_argument("--build-only", action="store_true")
+    ap.add_argument("--norm", default="rms", help="ln | rms, for the norm kernels (cols = H)")
     a = ap.parse_args()
     libs = {}
     for v in a.variants:
@@ -61,6 +62,11 @@ def main():
         codes = torch.empty((n + 3) // 4, dtype=torch.uint8, device=dev)
         nb = 2 * b * n + (n + 3) // 4
         codes4 = torch.empty((n + 1) // 2, dtype=torch.uint8, device=dev)
+        rstd = torch.rand(R, device=dev) + 0.5
+        if "nbwd" in a.kernels or "swb" in a.kernels:
+            x2, y2 = torch.empty_like(x), torch.empty_like(x)
+        if "nbwd" in a.kernels:
+            y.copy_(synth.norm_input(R, a.cols, a.dtype, device=dev))
         codes3 = torch.empty((3 * n + 7) // 8, dtype=torch.uint8, device=dev)
         ak = 0 if a.act == "gelu" else 1
         fns = {("torch", "copy"): (lambda: (y.copy_(x), 0)[1], 2 * b * n)}
@@ -69,6 +75,23 @@ def main():
             if "fwd" in a.kernels:
                 fns[(name, "fwd")] = (lambda f=f: f(x.data_ptr(), y.data_ptr(), codes.data_ptr(), R, a.cols,
                                                     DT[a.dtype], sp), nb)
+            nrm = "msln" if a.norm == "ln" else "msrms"
+            if "nfwd" in a.kernels:
+                nf = getattr(lib, nrm + "_fwd")
+                fns[(name, "nfwd")] = (lambda nf=nf: nf(x.data_ptr(), y.data_ptr(), rstd.data_ptr(), R, a.cols, 1e-6,
+                                                        DT[a.dtype], sp), 2 * b * n + 4 * R)
+            if "nbwd" in a.kernels:
+                nbk = getattr(lib, nrm + "_bwd")
+                fns[(name, "nbwd")] = (lambda nbk=nbk: nbk(dy.data_ptr(), y.data_ptr(), rstd.data_ptr(), dx.data_ptr(), R,
+                                                           a.cols, DT[a.dtype], sp), 3 * b * n + 4 * R)
+            if "swf" in a.kernels:
+                fns[(name, "swf")] = (lambda lib=lib: lib.reswiglu2_fwd(x.data_ptr(), dy.data_ptr(), y.data_ptr(),
+                                                                        dx.data_ptr(), codes.data_ptr(), R, a.cols,
+                                                                        DT[a.dtype], sp), 4 * b * n + (n + 3) // 4)
+            if "swb" in a.kernels:
+                fns[(name, "swb")] = (lambda lib=lib: lib.reswiglu2_bwd(y.data_ptr(), dy.data_ptr(), dx.data_ptr(),
+                                                                        codes.data_ptr(), x2.data_ptr(), y2.data_ptr(),
+                                                                        R, a.cols, DT[a.dtype], sp), 5 * b * n + (n + 3) // 4)
             if "step4" in a.kernels:
                 fns[(name, "step4")] = (lambda lib=lib: lib.stepact_fwd(ak, 4, ctypes.addressof(THR4), x.data_ptr(),
                                                                       y.data_ptr(), codes4.data_ptr(), R, a.cols,
