@@ -29,7 +29,7 @@ for dt in ("f32", "bf16", "f16"):
             cb = torch.empty(c.numel() + 1, dtype=torch.uint8, device=dev)   # misaligned codes: simple kernels
             y, c = P.stepact_fwd(x, "silu", k, thr, codes=cb[1:])
             P.stepact_bwd(dy, c, k, lv)
-    for (R, H) in ((3, 7), (33, 768), (9, 4096), (5, 5120), (2, 40000)):
+    for (R, H) in ((3, 7), (33, 768), (9, 4096), (5, 5120), (2, 40000), (2, 65537), (1, 262144)):
         xn = synth.norm_input(R, H, dt).to(dev)
         gn = synth.grad_input(R, H, dt).to(dev)
         for fwd, bwd in ((P.msln_fwd, P.msln_bwd), (P.msrms_fwd, P.msrms_bwd)):
