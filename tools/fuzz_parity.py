@@ -168,6 +168,20 @@ def case_mixed(rng):
 FAMILIES = {"act": case_act, "norm": case_norm, "kbit": case_kbit, "swiglu": case_swiglu, "mixed": case_mixed}
 
 
+def run_cases(seed: int, n: int):
+    """n cases from seed (the pytest entry point); returns the failures."""
+    fails = []
+    for i in range(n):
+        s = seed * 1_000_003 + i
+        rng = np.random.default_rng(s)
+        fam = str(rng.choice(list(FAMILIES)))
+        try:
+            FAMILIES[fam](rng)
+        except Exception as e:
+            fails.append((fam, s, repr(e)[:300]))
+    return fails
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
