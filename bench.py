@@ -708,6 +708,76 @@ class Workload:
             setattr(self, k, None)
 
 
+class StreamWorkload:
+    """The step as a training stream runs it: the four launches back to back
+    on one stream, no flush and no event between them, so each kernel's launch
+    and prologue overlap the previous one's drain (programmatic dependent
+    launch, csrc/common.cuh).  Two buffer sets: step s runs the forwards on
+    set s % 2 and the backwards on set (s + 1) % 2, consuming the codes, y and
+    rstd that the forwards wrote one step earlier -- every kernel's inputs
+    were last touched at least a whole step (> 2 x L2 bytes at every config)
+    before, so nothing is served from L2 that training would not also find
+    cold.  The activation inputs of the two sets are separate copies, too."""
+
+    def __init__(self, w: "Workload"):
+        self.w = w
+        clone = lambda t: t.clone()  # noqa: E731
+        self.x = [w.x, clone(w.x)]
+        self.dy = [w.dy, clone(w.dy)]
+        self.xn = [w.xn, clone(w.xn)]
+        self.gn = [w.gn, clone(w.gn)]
+        self.codes = [w.codes, torch.empty_like(w.codes)]
+        self.yn = [w.yn, torch.empty_like(w.yn)]
+        self.rstd = [w.rstd, torch.empty_like(w.rstd)]
+        s, eps = w.stream, w.eps
+        self.launch = {
+            "norm_fwd": lambda a: w.norm_fwd(self.xn[a], eps, y=self.yn[a], rstd=self.rstd[a], stream=s),
+            "act_fwd": lambda a: w.act_fwd(self.x[a], y=w.y, codes=self.codes[a], stream=s),
+            "act_bwd": lambda a: w.act_bwd(self.dy[a], self.codes[a], dx=w.dx, stream=s),
+            "norm_bwd": lambda a: w.norm_bwd(self.gn[a], self.yn[a], self.rstd[a], dx=w.dxn, stream=s),
+        }
+        for a in (0, 1):  # both sets hold a forward's outputs before the first backward reads them
+            self.launch["norm_fwd"](a)
+            self.launch["act_fwd"](a)
+
+    def step(self, s):
+        a, b = s & 1, (s + 1) & 1
+        self.launch["norm_fwd"](a)
+        self.launch["act_fwd"](a)
+        self.launch["act_bwd"](b)
+        self.launch["norm_bwd"](b)
+
+    def _time(self, body, n, warmup, world):
+        for i in range(max(3, warmup)):
+            body(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.w.stream)
+        for i in range(n):
+            body(i)
+        e1.record(self.w.stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        return e0.elapsed_time(e1)
+
+    def timed_steps(self, steps, warmup, world):
+        """ms for `steps` steps between one event pair (after W warm-up steps)."""
+        return self._time(self.step, steps, warmup, world)
+
+    def timed_kernel(self, k, launches, warmup, world):
+        """ms for `launches` back-to-back launches of one kernel, alternating
+        the two buffer sets (its inputs last touched one launch earlier, more
+        than L2's capacity before)."""
+        return self._time(lambda i: self.launch[k](i & 1), launches, warmup, world)
+
+    def free(self):
+        self.x = self.dy = self.xn = self.gn = self.codes = self.yn = self.rstd = None
+
+
 def gather_floats(vals, world, cdev):
     t = torch.tensor(vals, dtype=torch.float64, device=cdev)
     if world == 1:
@@ -798,6 +868,12 @@ def main(argv=None):
     per_kernel = w.timed(flush, flush_sink, args.steps, args.warmup, world, sampler)
     clocks = sampler.stop()
 
+    sw = StreamWorkload(w)
+    stream_ms = sw.timed_steps(args.steps, args.warmup, world)
+    stream_kms = {k: sw.timed_kernel(k, args.steps, args.warmup, world) / args.steps for k in KERNELS}
+    sw.free()
+    del sw
+
     total_ms = sum(sum(v) for v in per_kernel.values())
     nbytes = w.nbytes
     step_bytes = sum(nbytes.values())
@@ -808,6 +884,21 @@ def main(argv=None):
     value = aggregate(bytes_all, ms_all, args.steps)
 
     peak, peak_src = measured_hbm_peak()
+
+    sparts = gather_floats([stream_ms], world, cdev)
+    s_max = max(p[0] for p in sparts)
+    stream_line = {
+        "value": round(aggregate(bytes_all, [p[0] for p in sparts], args.steps), 1), "unit": "GB/s",
+        "ms_per_step": round(s_max / args.steps, 4),
+        "fraction_of_measured_peak": round(aggregate(bytes_all, [p[0] for p in sparts], args.steps) / world / peak, 4),
+        "pdl": os.environ.get("LMBP_PDL", "1")[:1] != "0",
+        "kernels": {k: {"us": round(stream_kms[k] * 1e3, 2),
+                        "GB/s": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9, 1),
+                        "frac": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
+        "protocol": "K steps back to back between one CUDA event pair, no flush; forwards on buffer set s%2, "
+                    "backwards on set (s+1)%2 (inputs last touched a step earlier); per-kernel: K back-to-back "
+                    "launches alternating the two sets between one event pair",
+    }
 
     kern = {}
     for k in kernels:
@@ -935,6 +1026,7 @@ def main(argv=None):
                        "parallelism": f"dp{world} (rows per rank, no data-path collective)",
                        "dist_backend": backend if world > 1 else None,
                        "devices": min(world, ndev)},
+            "stream": stream_line,
             "roofline": roofline, "rw_model": rw_model, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),

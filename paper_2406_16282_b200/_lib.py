@@ -59,12 +59,20 @@ def lib() -> ctypes.CDLL:
     """The loaded liblmbp.so.  Raises if it is absent -- never falls back."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise ImportError(f"liblmbp.so not found at {LIB}; run `python -m paper_2406_16282_b200.build` "
+        # LMBP_LIBRARY: a tuning build of the same sources with extra -D
+        # defines (build.build_variant, built without the fitter) for A/B runs
+        # of bench.py; the product library otherwise.
+        path = os.environ.get("LMBP_LIBRARY") or LIB
+        if not os.path.exists(path):
+            raise ImportError(f"liblmbp.so not found at {path}; run `python -m paper_2406_16282_b200.build` "
                               "(no CPU fallback exists)")
-        L = ctypes.CDLL(LIB)
+        L = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
-            f = getattr(L, name)
+            f = getattr(L, name, None)
+            if f is None and path != LIB and name.startswith("lmbp_fit"):
+                continue
+            if f is None:
+                raise ImportError(f"{path} does not export {name}")
             f.restype, f.argtypes = res, args
         _lib = L
     return _lib

@@ -2,6 +2,7 @@
 // Synchronous argument validation, dtype dispatch, status codes.  No
 // allocation, no synchronisation, nothing printed, no exceptions escape.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/lmbp.h"
@@ -15,6 +16,14 @@ int sm_count() {
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
   return n;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("LMBP_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 static int check_shape(int64_t rows, int64_t cols) {

@@ -46,6 +46,7 @@ __device__ void act_fwd_tail(const T *x, T *y, uint8_t *codes, int64_t j0, int64
 // Forward, scalar path (any alignment): one code byte (4 elements) per thread.
 template <typename T, int A, bool kPrecise>
 __global__ void __launch_bounds__(256) act_fwd_scalar(const T *x, T *y, uint8_t *codes, int64_t n) {
+  pdl_enter();
   const int64_t nbytes = (n + 3) >> 2;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * blockDim.x) {
     uint32_t byte = 0;
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(256) act_fwd_scalar(const T *x, T *y, uint8_t 
 template <typename T, int A, int U>
 __global__ void __launch_bounds__(256) act_bwd_vec(const uint4 *dy, const uint8_t *codes, uint4 *dx, int64_t nvec,
                                                    int64_t n) {
+  pdl_enter();
   constexpr int kVec = Traits<T>::kVec;
   const CodeWord<T> *cw = reinterpret_cast<const CodeWord<T> *>(codes);
   const int64_t tile = (int64_t)blockDim.x * U;
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(256) act_bwd_vec(const uint4 *dy, const uint8_
 
 template <typename T, int A>
 __global__ void __launch_bounds__(256) act_bwd_scalar(const T *dy, const uint8_t *codes, T *dx, int64_t n) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t cj = (codes[j >> 2] >> (2 * (j & 3))) & 3u;
     dx[j] = from_f32<T>(__fmul_rn(to_f32<T>(dy[j]), level<A>(cj)));
@@ -308,7 +311,7 @@ static cudaError_t act_fwd_t(const void *x, void *y, uint8_t *codes, int64_t n, 
     static const int occ = occupancy(kern, kActThreads);
     const int64_t want = cdiv(cdiv(n, 4), kActThreads);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
-    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y), codes, n);
+    launch_k(kern, grid, kActThreads, 0, s, reinterpret_cast<const T *>(x), reinterpret_cast<T *>(y), codes, n);
   }
   return cudaGetLastError();
 }
@@ -333,14 +336,14 @@ static cudaError_t act_bwd_t(const void *dy, const uint8_t *codes, void *dx, int
     const int64_t nvec = n / kVec;
     const int64_t want = cdiv(nvec, (int64_t)kActThreads * kActUnroll);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
-    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const uint4 *>(dy), codes, reinterpret_cast<uint4 *>(dx),
+    launch_k(kern, grid, kActThreads, 0, s, reinterpret_cast<const uint4 *>(dy), codes, reinterpret_cast<uint4 *>(dx),
                                       nvec, n);
   } else {
     auto kern = act_bwd_scalar<T, A>;
     static const int occ = occupancy(kern, kActThreads);
     const int64_t want = cdiv(n, kActThreads);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
-    kern<<<grid, kActThreads, 0, s>>>(reinterpret_cast<const T *>(dy), codes, reinterpret_cast<T *>(dx), n);
+    launch_k(kern, grid, kActThreads, 0, s, reinterpret_cast<const T *>(dy), codes, reinterpret_cast<T *>(dx), n);
   }
   return cudaGetLastError();
 }

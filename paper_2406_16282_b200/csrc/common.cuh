@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 
 #include "constants.cuh"
 
@@ -175,6 +176,50 @@ struct StepTable {
 
 // Device attribute helpers (host side).
 int sm_count();
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+).  Every hot-path kernel is launched
+// with programmatic stream serialization, so when it follows another kernel
+// on the stream its CTAs may be scheduled before that kernel has finished
+// (once every CTA of it has executed launch_dependents or exited) and run
+// their prologue -- launch, barrier init, the 128 KB table copy -- under the
+// previous kernel's drain.  pdl_wait() (griddepcontrol.wait) then blocks
+// until the previous grid has COMPLETED and its memory is visible, so it sits
+// before the first global access that could depend on it: every load of an
+// input and every store of an output (a store could race a read of the
+// previous kernel: WAR).  Only immutable data (the module's constant tables,
+// kernel parameters) is touched before it.  Launched without the attribute
+// (LMBP_PDL=0, or after a non-kernel stream operation) both instructions are
+// no-ops and the stream serialises as usual.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Entry of a kernel with no prologue worth overlapping.
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+bool pdl_enabled();  // abi.cu: LMBP_PDL environment variable, read once (default on)
+
+// Launch `kernel` on `s` with programmatic stream serialization (when
+// enabled).  Like <<<>>>, a failed launch leaves its error in the runtime's
+// last-error slot: callers return cudaGetLastError().
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Opt a kernel into `bytes` of dynamic shared memory on the current device,
 // once per (kernel instantiation, device).  Function attributes are per

@@ -231,6 +231,10 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
         for (int q = 0; q < 4; ++q)
           bulk_g2s(smem_all + q * (kTab16Bytes / 4), src + q * (kTab16Bytes / 4), kTab16Bytes / 4, tab_bar);
       }
+      // The table is module data; everything below reads inputs (PDL: wait
+      // for the previous grid here, common.cuh).
+      pdl_wait();
+      pdl_trigger();
       int k = 0;
       int64_t unit = blockIdx.x;
       uint32_t clc_phase = 0;
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(EwShape<Op>::kThreads, MinBlocksOf<Op>::value)
     asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");  // consumers only
   }
   if constexpr (Tab16Of<Op>::value) mbar_wait(tab_bar, 0);
+  pdl_wait();  // consumers store outputs (and the leftover path loads inputs) only after it
   for (int k = 0;; ++k) {
     const int s = k % S;
     mbar_wait(&full[s], (uint32_t)(k / S) & 1u);
@@ -373,7 +378,7 @@ cudaError_t launch_ew(const typename ParamsOf<Op>::type &p_in, cudaStream_t stre
   const int64_t units = (items + LMBP_EW_UNIT - 1) / LMBP_EW_UNIT;
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
   const int grid = (int)units;  // CTAs beyond the resident ones are taken over via CLC
-  kern<<<grid, Sh::kThreads, Sh::kSmem, stream>>>(p);
+  launch_k(kern, grid, Sh::kThreads, Sh::kSmem, stream, p);
   return cudaGetLastError();
 }
 

@@ -71,6 +71,7 @@ __device__ __forceinline__ float2 team_sum2(float2 v, float2 *buf) {
 template <typename T, int NORM, int V, bool kWarpTeam>
 __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint4 *x, uint4 *y, float *rstd,
                                                      int64_t rows, int nvec, int cols, float eps) {
+  pdl_enter();
   constexpr int kVec = Traits<T>::kVec;
   __shared__ float red[2][32];
   const int team = kWarpTeam ? 32 : (int)blockDim.x;
@@ -147,6 +148,7 @@ template <typename T, int NORM, int V, bool kWarpTeam>
 __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint4 *dy, const uint4 *__restrict__ y,
                                                      const float *__restrict__ rstd, uint4 *dx, int64_t rows,
                                                      int nvec, int cols) {
+  pdl_enter();
   constexpr int kVec = Traits<T>::kVec;
   __shared__ float2 red[2][32];
   const int team = kWarpTeam ? 32 : (int)blockDim.x;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(512) norm_tma(const uint4 *a, const uint4 *b, 
     GW = (int64_t)gridDim.x * W;
     row_end = rows;
   }
+  pdl_enter();
   const float fcols = (float)cols;
   if (lane == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
@@ -400,6 +403,7 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_enter();
 
   if (warp == W) {  // producer
     if (lane == 0) {
@@ -620,7 +624,7 @@ static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const v
   if (e != cudaSuccess) return e;
   const int64_t units = (rows + LMBP_ROW_UNIT - 1) / LMBP_ROW_UNIT;
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
-  kern<<<(int)units, (rp.warps + 1) * 32, rp.smem, s>>>(reinterpret_cast<const uint4 *>(a),
+  launch_k(kern, (int)units, (rp.warps + 1) * 32, rp.smem, s, reinterpret_cast<const uint4 *>(a),
                                                         reinterpret_cast<const uint4 *>(b), rstd_in,
                                                         reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec,
                                                         (int)cols, eps, rp.stages);
@@ -686,7 +690,7 @@ static cudaError_t launch_norm_tma(const TmaPlan &tp, const void *a, const void 
   const int64_t want = (rows + tp.warps - 1) / tp.warps;
   const int grid = rpw > 0 ? (int)std::max<int64_t>(1, (rows + (int64_t)tp.warps * rpw - 1) / ((int64_t)tp.warps * rpw))
                            : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
-  kern<<<grid, threads, tp.smem, s>>>(reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), rstd_in,
+  launch_k(kern, grid, threads, tp.smem, s, reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), rstd_in,
                                       reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec, (int)cols, eps, tp.stages,
                                       rpw);
   return cudaGetLastError();
@@ -698,6 +702,7 @@ static cudaError_t launch_norm_tma(const TmaPlan &tp, const void *a, const void 
 template <typename T, int NORM>
 __global__ void __launch_bounds__(256) norm_fwd_scalar(const T *x, T *y, float *rstd, int64_t rows, int64_t cols,
                                                        float eps) {
+  pdl_enter();
   __shared__ float red[2][32];
   const float fcols = (float)cols;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -727,6 +732,7 @@ __global__ void __launch_bounds__(256) norm_fwd_scalar(const T *x, T *y, float *
 template <typename T, int NORM>
 __global__ void __launch_bounds__(256) norm_bwd_scalar(const T *dy, const T *y, const float *rstd, T *dx,
                                                        int64_t rows, int64_t cols) {
+  pdl_enter();
   __shared__ float2 red[2][32];
   const float fcols = (float)cols;
   int it = 0;
@@ -826,7 +832,7 @@ static void launch_rows(K kernel, int64_t rows, int rows_per_block, int threads,
   const int64_t want = (rows + rows_per_block - 1) / rows_per_block;
   const int64_t cap = (rows_per_block == 1 || !persistent) ? (int64_t)0x7fffffff : (int64_t)sm_count() * occ;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
-  kernel<<<grid, threads, 0, s>>>(args...);
+  launch_k(kernel, grid, threads, 0, s, args...);
 }
 
 template <typename T, int NORM, int V, bool W>

@@ -69,6 +69,7 @@ template <typename TO, int NORM, int V, bool kWarpTeam>
 __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_mixed_vec(const uint4 *x, uint4 *y, float *rstd,
                                                                            int64_t rows, int ngrp, int cols,
                                                                            float eps) {
+  pdl_enter();
   __shared__ float red[2][32];
   const int team = kWarpTeam ? 32 : (int)blockDim.x;
   const int tid = kWarpTeam ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
@@ -145,6 +146,7 @@ template <typename TO, int NORM, int V, bool kWarpTeam>
 __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(const uint4 *dy, const uint4 *__restrict__ y,
                                                                            const float *__restrict__ rstd, uint4 *dx,
                                                                            int64_t rows, int ngrp, int cols) {
+  pdl_enter();
   __shared__ float2 red[2][32];
   const int team = kWarpTeam ? 32 : (int)blockDim.x;
   const int tid = kWarpTeam ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(cons
 template <typename TO, int NORM>
 __global__ void __launch_bounds__(256) norm_fwd_mixed_scalar(const float *x, TO *y, float *rstd, int64_t rows,
                                                              int64_t cols, float eps) {
+  pdl_enter();
   __shared__ float red[2][32];
   const float fcols = (float)cols;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(256) norm_fwd_mixed_scalar(const float *x, TO 
 template <typename TO, int NORM>
 __global__ void __launch_bounds__(256) norm_bwd_mixed_scalar(const TO *dy, const TO *y, const float *rstd, float *dx,
                                                              int64_t rows, int64_t cols) {
+  pdl_enter();
   __shared__ float2 red[2][32];
   const float fcols = (float)cols;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -310,7 +314,7 @@ cudaError_t fwd_mixed_t(const float *x, void *y, float *rstd, int64_t rows, int6
       static const int occ = occupancy_mixed(kern, 256);
       const int64_t want = (rows + 7) / 8;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
-      kern<<<grid, 256, 0, s>>>(xv, yv, rstd, rows, p.ngrp, (int)cols, eps);
+      launch_k(kern, grid, 256, 0, s, xv, yv, rstd, rows, p.ngrp, (int)cols, eps);
     };
     switch (p.V) {
       case 1: launch(norm_fwd_mixed_vec<TO, NORM, 1, true>); break;
@@ -320,10 +324,10 @@ cudaError_t fwd_mixed_t(const float *x, void *y, float *rstd, int64_t rows, int6
     }
   } else if (p.vec) {
     const int grid = (int)std::min<int64_t>(rows, 0x7fffffff);  // one CTA per row; the hardware balances
-    norm_fwd_mixed_vec<TO, NORM, 4, false><<<grid, p.team, 0, s>>>(xv, yv, rstd, rows, p.ngrp, (int)cols, eps);
+    launch_k(norm_fwd_mixed_vec<TO, NORM, 4, false>, grid, p.team, 0, s, xv, yv, rstd, rows, p.ngrp, (int)cols, eps);
   } else {
     const int grid = (int)std::min<int64_t>(rows, (int64_t)sm_count() * 8);
-    norm_fwd_mixed_scalar<TO, NORM><<<grid, 256, 0, s>>>(x, reinterpret_cast<TO *>(y), rstd, rows, cols, eps);
+    launch_k(norm_fwd_mixed_scalar<TO, NORM>, grid, 256, 0, s, x, reinterpret_cast<TO *>(y), rstd, rows, cols, eps);
   }
   return cudaGetLastError();
 }
@@ -340,7 +344,7 @@ cudaError_t bwd_mixed_t(const void *dy, const void *y, const float *rstd, float 
       static const int occ = occupancy_mixed(kern, 256);
       const int64_t want = (rows + 7) / 8;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
-      kern<<<grid, 256, 0, s>>>(gv, yv, rstd, dv, rows, p.ngrp, (int)cols);
+      launch_k(kern, grid, 256, 0, s, gv, yv, rstd, dv, rows, p.ngrp, (int)cols);
     };
     switch (p.V) {
       case 1: launch(norm_bwd_mixed_vec<TO, NORM, 1, true>); break;
@@ -350,10 +354,10 @@ cudaError_t bwd_mixed_t(const void *dy, const void *y, const float *rstd, float 
     }
   } else if (p.vec) {
     const int grid = (int)std::min<int64_t>(rows, 0x7fffffff);
-    norm_bwd_mixed_vec<TO, NORM, 4, false><<<grid, p.team, 0, s>>>(gv, yv, rstd, dv, rows, p.ngrp, (int)cols);
+    launch_k(norm_bwd_mixed_vec<TO, NORM, 4, false>, grid, p.team, 0, s, gv, yv, rstd, dv, rows, p.ngrp, (int)cols);
   } else {
     const int grid = (int)std::min<int64_t>(rows, (int64_t)sm_count() * 8);
-    norm_bwd_mixed_scalar<TO, NORM><<<grid, 256, 0, s>>>(reinterpret_cast<const TO *>(dy),
+    launch_k(norm_bwd_mixed_scalar<TO, NORM>, grid, 256, 0, s, reinterpret_cast<const TO *>(dy),
                                                          reinterpret_cast<const TO *>(y), rstd, dx, rows, cols);
   }
   return cudaGetLastError();

@@ -94,6 +94,7 @@ __device__ __forceinline__ void store8(T *p, int64_t g, bool vec, const float *f
 template <typename T, int A, bool kPrecise, int K>
 __global__ void __launch_bounds__(256) stepact_fwd_k(const T *x, T *y, uint8_t *codes, int64_t n, StepTable tab,
                                                      bool vec) {
+  pdl_enter();
   const int64_t groups = n / 8;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
     float f[8];
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(256) stepact_fwd_k(const T *x, T *y, uint8_t *
 template <typename T, int K>
 __global__ void __launch_bounds__(256) stepact_bwd_k(const T *dy, const uint8_t *codes, T *dx, int64_t n,
                                                      StepTable tab, bool vec) {
+  pdl_enter();
   __shared__ float lvl[16];
   if (threadIdx.x < (1 << K)) lvl[threadIdx.x] = tab.lvl[threadIdx.x];
   __syncthreads();
@@ -482,7 +484,7 @@ static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t
       return launch_ew<StepFwdOp<T, A, kPrecise, K>>(p, s);
     }
   }
-  stepact_fwd_k<T, A, kPrecise, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(x),
+  launch_k(stepact_fwd_k<T, A, kPrecise, K>, step_grid(n / 8), 256, 0, s, reinterpret_cast<const T *>(x),
                                                                      reinterpret_cast<T *>(y), codes, n, tab, vec);
   return cudaGetLastError();
 }
@@ -503,7 +505,7 @@ static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx,
       return launch_ew<StepBwdOp<T, K>>(p, s);
     }
   }
-  stepact_bwd_k<T, K><<<step_grid(n / 8), 256, 0, s>>>(reinterpret_cast<const T *>(dy), codes,
+  launch_k(stepact_bwd_k<T, K>, step_grid(n / 8), 256, 0, s, reinterpret_cast<const T *>(dy), codes,
                                                         reinterpret_cast<T *>(dx), n, tab, vec);
   return cudaGetLastError();
 }

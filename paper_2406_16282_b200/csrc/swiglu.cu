@@ -129,6 +129,7 @@ struct SwiGluBwdOp {
 template <typename T, bool kPrecise>
 __global__ void __launch_bounds__(256) swiglu_fwd_scalar(const T *g, const T *u, T *h, T *a, uint8_t *codes,
                                                          int64_t n) {
+  pdl_enter();
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (n + 3) / 4;
        b += (int64_t)gridDim.x * blockDim.x) {
     uint32_t byte = 0;
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(256) swiglu_fwd_scalar(const T *g, const T *u,
 template <typename T>
 __global__ void __launch_bounds__(256) swiglu_bwd_scalar(const T *dh, const T *u, const T *a, const uint8_t *codes,
                                                          T *dg, T *du, int64_t n) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t cj = (codes[j >> 2] >> (2 * (j & 3))) & 3u;
     swiglu_bwd_elem<T>(to_f32<T>(dh[j]), to_f32<T>(u[j]), to_f32<T>(a[j]), cj, dg[j], du[j]);
@@ -178,7 +180,7 @@ static cudaError_t swiglu_fwd_t(const void *g, const void *u, void *h, void *a, 
     p.n = n;
     return launch_ew<SwiGluFwdOp<T, kPrecise>>(p, s);
   }
-  swiglu_fwd_scalar<T, kPrecise><<<scalar_grid((n + 3) / 4), 256, 0, s>>>(
+  launch_k(swiglu_fwd_scalar<T, kPrecise>, scalar_grid((n + 3) / 4), 256, 0, s, 
       reinterpret_cast<const T *>(g), reinterpret_cast<const T *>(u), reinterpret_cast<T *>(h),
       reinterpret_cast<T *>(a), codes, n);
   return cudaGetLastError();
@@ -200,7 +202,7 @@ static cudaError_t swiglu_bwd_t(const void *dh, const void *u, const void *a, co
     p.n = n;
     return launch_ew<SwiGluBwdOp<T>>(p, s);
   }
-  swiglu_bwd_scalar<T><<<scalar_grid(n), 256, 0, s>>>(reinterpret_cast<const T *>(dh), reinterpret_cast<const T *>(u),
+  launch_k(swiglu_bwd_scalar<T>, scalar_grid(n), 256, 0, s, reinterpret_cast<const T *>(dh), reinterpret_cast<const T *>(u),
                                                        reinterpret_cast<const T *>(a), codes, reinterpret_cast<T *>(dg),
                                                        reinterpret_cast<T *>(du), n);
   return cudaGetLastError();
