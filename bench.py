@@ -12,6 +12,12 @@ L2 is flushed (a read of 2 x L2) before every kernel, outside the events, so no
 kernel reads another's output from L2 (in training the whole network runs in
 between).  value = algorithmic bytes of all ranks / max-over-ranks device time.
 
+The `stream` key times the same step the way a training stream runs it: K
+steps back to back between one event pair, no flush, consecutive kernels
+overlapped by programmatic dependent launch, the backwards of step s reading
+what the forwards of step s-1 wrote (two buffer sets, so every input was last
+touched more than L2's capacity earlier).  DESIGN.md 5.10 and 6.
+
 Multi-GPU: one process per GPU; every rank processes its own batch of the
 configured shape (weak scaling, data-parallel, no collective on the data path);
 NCCL is used only for the barrier and the max/sum of timings.
@@ -729,12 +735,13 @@ class StreamWorkload:
         self.codes = [w.codes, torch.empty_like(w.codes)]
         self.yn = [w.yn, torch.empty_like(w.yn)]
         self.rstd = [w.rstd, torch.empty_like(w.rstd)]
-        s, eps = w.stream, w.eps
+        eps = w.eps
+        self.s = w.stream      # the launch stream (the capture stream while a graph is recorded)
         self.launch = {
-            "norm_fwd": lambda a: w.norm_fwd(self.xn[a], eps, y=self.yn[a], rstd=self.rstd[a], stream=s),
-            "act_fwd": lambda a: w.act_fwd(self.x[a], y=w.y, codes=self.codes[a], stream=s),
-            "act_bwd": lambda a: w.act_bwd(self.dy[a], self.codes[a], dx=w.dx, stream=s),
-            "norm_bwd": lambda a: w.norm_bwd(self.gn[a], self.yn[a], self.rstd[a], dx=w.dxn, stream=s),
+            "norm_fwd": lambda a: w.norm_fwd(self.xn[a], eps, y=self.yn[a], rstd=self.rstd[a], stream=self.s),
+            "act_fwd": lambda a: w.act_fwd(self.x[a], y=w.y, codes=self.codes[a], stream=self.s),
+            "act_bwd": lambda a: w.act_bwd(self.dy[a], self.codes[a], dx=w.dx, stream=self.s),
+            "norm_bwd": lambda a: w.norm_bwd(self.gn[a], self.yn[a], self.rstd[a], dx=w.dxn, stream=self.s),
         }
         for a in (0, 1):  # both sets hold a forward's outputs before the first backward reads them
             self.launch["norm_fwd"](a)
@@ -756,8 +763,10 @@ class StreamWorkload:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(self.w.stream)
+        h0 = time.perf_counter()
         for i in range(n):
             body(i)
+        self.last_host_s = time.perf_counter() - h0   # host time to enqueue the n units
         e1.record(self.w.stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -767,6 +776,31 @@ class StreamWorkload:
     def timed_steps(self, steps, warmup, world):
         """ms for `steps` steps between one event pair (after W warm-up steps)."""
         return self._time(self.step, steps, warmup, world)
+
+    def graph(self, body, n):
+        """A CUDA graph of body(0) .. body(n - 1) (n even: both buffer sets),
+        recorded from the same launches (PDL launches become programmatic
+        edges), so replaying it costs one host call per n launches."""
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(self.w.dev)
+        cs.wait_stream(self.w.stream)
+        with torch.cuda.graph(g, stream=cs):
+            self.s = cs
+            for i in range(n):
+                body(i)
+        self.s = self.w.stream
+        self.w.stream.wait_stream(cs)
+        return g
+
+    def timed_graph(self, body, per_graph, total, warmup, world):
+        """ms for `total` units (launches or steps) replayed from a graph of
+        `per_graph` units, between one event pair."""
+        g = self.graph(body, per_graph)
+        reps = max(1, total // per_graph)
+        with torch.cuda.stream(self.w.stream):
+            ms = self._time(lambda i: g.replay(), reps, max(1, warmup // per_graph), world)
+        del g
+        return ms * total / (reps * per_graph)
 
     def timed_kernel(self, k, launches, warmup, world):
         """ms for `launches` back-to-back launches of one kernel, alternating
@@ -870,7 +904,12 @@ def main(argv=None):
 
     sw = StreamWorkload(w)
     stream_ms = sw.timed_steps(args.steps, args.warmup, world)
+    t_host = sw.last_host_s
     stream_kms = {k: sw.timed_kernel(k, args.steps, args.warmup, world) / args.steps for k in KERNELS}
+    # the same launches replayed from CUDA graphs (no per-launch host cost)
+    graph_ms = sw.timed_graph(sw.step, 2, args.steps, args.warmup, world)
+    graph_kms = {k: sw.timed_graph(lambda i, k=k: sw.launch[k](i & 1), 8, args.steps, args.warmup, world)
+                 / args.steps for k in KERNELS}
     sw.free()
     del sw
 
@@ -887,11 +926,24 @@ def main(argv=None):
 
     sparts = gather_floats([stream_ms], world, cdev)
     s_max = max(p[0] for p in sparts)
+    gparts = gather_floats([graph_ms], world, cdev)
+    graph_line = {
+        "value": round(aggregate(bytes_all, [p[0] for p in gparts], args.steps), 1), "unit": "GB/s",
+        "ms_per_step": round(max(p[0] for p in gparts) / args.steps, 4),
+        "fraction_of_measured_peak": round(aggregate(bytes_all, [p[0] for p in gparts], args.steps) / world / peak, 4),
+        "kernels": {k: {"us": round(graph_kms[k] * 1e3, 2),
+                        "GB/s": round(nbytes[k] / (graph_kms[k] / 1e3) / 1e9, 1),
+                        "frac": round(nbytes[k] / (graph_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
+        "protocol": "the stream protocol's launches captured in CUDA graphs (2 steps, or 8 launches of one kernel, "
+                    "per graph; PDL launches become programmatic edges) and replayed between one event pair",
+    }
     stream_line = {
         "value": round(aggregate(bytes_all, [p[0] for p in sparts], args.steps), 1), "unit": "GB/s",
         "ms_per_step": round(s_max / args.steps, 4),
         "fraction_of_measured_peak": round(aggregate(bytes_all, [p[0] for p in sparts], args.steps) / world / peak, 4),
         "pdl": os.environ.get("LMBP_PDL", "1")[:1] != "0",
+        "host_enqueue_ms_per_step": round(1e3 * t_host / args.steps, 4),
+        "graph": graph_line,
         "kernels": {k: {"us": round(stream_kms[k] * 1e3, 2),
                         "GB/s": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9, 1),
                         "frac": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
