@@ -821,6 +821,41 @@ def gather_floats(vals, world, cdev):
     return [p.tolist() for p in parts]
 
 
+OUTPUTS = ("y", "codes", "dx", "yn", "rstd", "dxn")
+
+
+def row_slices(cfg, r0, r1):
+    """Element (byte, for codes) ranges of rows [r0, r1) in each flat output
+    of a Workload (F % 4 == 0, so a row block's codes are whole bytes)."""
+    F, H = cfg["F"], cfg["H"]
+    return {"y": (r0 * F, r1 * F), "codes": (r0 * F // 4, r1 * F // 4), "dx": (r0 * F, r1 * F),
+            "yn": (r0 * H, r1 * H), "rstd": (r0, r1), "dxn": (r0 * H, r1 * H)}
+
+
+def output_checksums(w, r0, r1, base_row):
+    """Position-weighted int64 checksums of the bytes of rows [r0, r1) of
+    every output of `w` (whose first row is global row `base_row`); the weights
+    depend on the byte's global position, so equal checksums across shardings
+    mean equal bytes in place (with overwhelming probability)."""
+    sl = row_slices(w.cfg, r0 - base_row, r1 - base_row)
+    g0 = row_slices(w.cfg, r0, r1)
+    M = 2147483647
+    out = []
+    for name in OUTPUTS:
+        t = getattr(w, name).reshape(-1)
+        lo, hi = sl[name]
+        eb = t.element_size()
+        raw = t[lo:hi].view(torch.uint8)
+        p0 = g0[name][0] * eb
+        acc = 0
+        for c in range(0, raw.numel(), 1 << 26):   # 64 MB chunks bound the int64 temporaries
+            b = raw[c:c + (1 << 26)].to(torch.int64)
+            pos = torch.arange(p0 + c, p0 + c + b.numel(), device=b.device, dtype=torch.int64)
+            acc = (acc + int((((b + 1) * ((pos * 2654435761) % 1000003 + 1)) % M).sum().item())) % M
+        out.append(float(acc))                      # < 2^31: exact in the float64 gather
+    return out
+
+
 def strong_section(P, args, world, rank, dev, stream, flush, sink, cdev):
     """north_star / SURVEY 8(e): the strong-scaling configuration (C5,
     LLaMA-13B shapes) with its R rows split into contiguous blocks, rank r
@@ -833,10 +868,12 @@ def strong_section(P, args, world, rank, dev, stream, flush, sink, cdev):
     pk = w.timed(flush, sink, args.strong_steps, 3, world)
     ms = sum(sum(v) for v in pk.values())
     nb = sum(w.nbytes.values())
-    parts = gather_floats([ms, float(nb), float(row0), float(R)], world, cdev)
+    sums = output_checksums(w, row0, row0 + R, row0)
+    parts = gather_floats([ms, float(nb), float(row0), float(R)] + sums, world, cdev)
     w.free()
     torch.cuda.empty_cache()
     t1 = None
+    shard_check = None
     if world == 1:
         t1 = ms / args.strong_steps
     else:
@@ -844,6 +881,14 @@ def strong_section(P, args, world, rank, dev, stream, flush, sink, cdev):
             w1 = Workload(P, cfg, 0, cfg["R"], dev, stream, args.eps)
             pk1 = w1.timed(flush, sink, args.strong_steps, 3, 1)
             t1 = sum(sum(v) for v in pk1.values()) / args.strong_steps
+            # 8(e): the one-GPU run's outputs, checksummed over every rank's
+            # row block, must equal what that rank computed on its shard
+            mism = []
+            for r, p in enumerate(parts):
+                a, n = int(p[2]), int(p[3])
+                ref = output_checksums(w1, a, a + n, 0)
+                mism += [f"rank{r}:{name}" for name, u, v in zip(OUTPUTS, p[4:], ref) if u != v]
+            shard_check = {"outputs": list(OUTPUTS), "bitwise_equal_to_one_gpu": not mism, "mismatches": mism}
             w1.free()
             torch.cuda.empty_cache()
         torch.distributed.barrier()
@@ -853,7 +898,9 @@ def strong_section(P, args, world, rank, dev, stream, flush, sink, cdev):
     out.update({"config": f"{args.strong_config}: {cfg['desc']}", "rows_total": cfg["R"],
                 "shards": [[int(p[2]), int(p[3])] for p in parts], "steps": args.strong_steps,
                 "partition": "contiguous row blocks, rank r owns rows [r*R/N, (r+1)*R/N); no data-path collective",
-                "t1": "rank 0 alone on all rows, same run" if world > 1 else "this run"})
+                "t1": "rank 0 alone on all rows, same run" if world > 1 else "this run",
+                "shard_invariance": shard_check,
+                "checksums": "per rank and output, position-weighted byte sums all-gathered with the timings"})
     return out
 
 
