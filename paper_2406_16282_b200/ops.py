@@ -45,9 +45,10 @@ def _need(t: torch.Tensor, name: str) -> torch.Tensor:
 def _stream(stream, dev: torch.device) -> int:
     if stream is None:
         stream = torch.cuda.current_stream(dev)
-    elif isinstance(stream, torch.cuda.Stream) and stream.device != dev:
-        raise ValueError(f"stream is on {stream.device}, tensors on {dev}")
-    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+    elif isinstance(stream, torch.cuda.Stream):
+        if stream.device != dev:
+            raise ValueError(f"stream is on {stream.device}, tensors on {dev}")
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
 def _device(fn: str, *ts: torch.Tensor) -> torch.device:
@@ -60,19 +61,37 @@ def _device(fn: str, *ts: torch.Tensor) -> torch.device:
     return dev
 
 
+_ENTRY = {}
+
+
+def _entry(fn: str):
+    f = _ENTRY.get(fn)
+    if f is None:
+        f = _ENTRY[fn] = getattr(lib(), fn)
+    return f
+
+
 def _launch(fn: str, dev: torch.device, stream, *args) -> None:
-    """Call entry point fn(*args, stream) with dev current; raise on a status."""
+    """Call entry point fn(*args, stream) with dev current; raise on a status.
+    (The device switch is skipped when dev already is the current device: it
+    is most of the host cost of a call.)"""
     s = _stream(stream, dev)
-    with torch.cuda.device(dev):
-        check(fn, getattr(lib(), fn)(*args, s))
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        status = _entry(fn)(*args, s)
+    else:
+        with torch.cuda.device(dev):
+            status = _entry(fn)(*args, s)
+    if status:
+        check(fn, status)
 
 
 def _act_fwd(fn: str, x, y, codes, stream):
     _need(x, "x")
     y = torch.empty_like(x) if y is None else _need(y, "y")
     n = x.numel()
-    codes = torch.empty(codes_bytes(n), dtype=torch.uint8, device=x.device) if codes is None else _need(codes, "codes")
-    if y.shape != x.shape or y.dtype != x.dtype or codes.numel() != codes_bytes(n):
+    nc = codes_bytes(n)
+    codes = torch.empty(nc, dtype=torch.uint8, device=x.device) if codes is None else _need(codes, "codes")
+    if y.shape != x.shape or y.dtype != x.dtype or codes.numel() != nc:
         raise ValueError(f"{fn}: shape/dtype mismatch")
     rows, cols = _rc(x)
     if n == 0:
@@ -87,8 +106,9 @@ def _act_bwd(fn: str, dy, codes, dx, stream):
     _need(codes, "codes")
     dx = torch.empty_like(dy) if dx is None else _need(dx, "dx")
     n = dy.numel()
-    if codes.numel() != codes_bytes(n) or codes.dtype != torch.uint8:
-        raise ValueError(f"{fn}: codes must be uint8[{codes_bytes(n)}] (S:L174)")
+    nc = codes_bytes(n)
+    if codes.numel() != nc or codes.dtype != torch.uint8:
+        raise ValueError(f"{fn}: codes must be uint8[{nc}] (S:L174)")
     if dx.shape != dy.shape or dx.dtype != dy.dtype:
         raise ValueError(f"{fn}: shape/dtype mismatch")
     rows, cols = _rc(dy)
