@@ -488,6 +488,29 @@ def mixed_norm_section(P, cfg, R, dev, stream, flush, sink, peak, eps, iters=20)
     return out
 
 
+def graph_us(body, stream, per_graph=8, reps=8):
+    """Mean µs per launch of body(0) .. body(per_graph - 1) captured in one
+    CUDA graph (launches back to back, PDL edges kept) and replayed `reps`
+    times between one event pair.  `body` launches on the current stream."""
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(stream.device)
+    cs.wait_stream(stream)
+    with torch.cuda.graph(g, stream=cs):
+        for i in range(per_graph):
+            body(i)
+    stream.wait_stream(cs)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (reps * per_graph)
+
+
 def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     """the table-driven k-bit step activation on the
     config's activation tensor -- k = 2 with the paper's table (bitwise equal
@@ -496,6 +519,7 @@ def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     tab = tables.REGELU2 if cfg["act"] == "gelu" else tables.RESILU2
     b, n = x.element_size(), x.numel()
     y, dx = torch.empty_like(x), torch.empty_like(dy)
+    x2, dy2 = x.clone(), dy.clone()
     out = {}
     for k, thr, lv in ((2, tab["c"], tables.levels(tab)),
                        (3, [-3.0 + 1.0 * i for i in range(7)], [i / 7 for i in range(8)]),
@@ -518,9 +542,18 @@ def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
             torch.cuda.synchronize()
             ts.append(sum(a.elapsed_time(c) for a, c in evs) / iters * 1e3)
         nbytes = 2 * (2 * b * n + P.codes_bytes_k(n, k))
+        # in-stream: back-to-back launches from a graph, alternating two input
+        # / code sets (each launch's inputs last touched > L2 bytes earlier)
+        codes2 = torch.empty_like(codes)
+        cs, xs, dys = (codes, codes2), (x, x2), (dy, dy2)
+        gf = graph_us(lambda i: P.stepact_fwd(xs[i & 1], tab["act"], k, thr, y=y, codes=cs[i & 1]), stream)
+        gb = graph_us(lambda i: P.stepact_bwd(dys[i & 1], cs[i & 1], k, lv, dx=dx), stream)
         out[f"k{k}"] = {"fwd_us": round(ts[0], 2), "bwd_us": round(ts[1], 2),
                         "GB/s": round(nbytes / (ts[0] + ts[1]) / 1e3, 1),
-                        "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / peak, 4)}
+                        "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / peak, 4),
+                        "graph_fwd_us": round(gf, 2), "graph_bwd_us": round(gb, 2),
+                        "graph_frac": round(nbytes / (gf + gb) / 1e3 / peak, 4)}
+        del codes2
     return out
 
 
