@@ -37,6 +37,13 @@
  *   LMBP_OK.  Faults during asynchronous execution surface at the caller's
  *   next synchronisation, as usual in CUDA.  Nothing is printed, no C++
  *   exception crosses the ABI.
+ * Launch.  Kernels are launched with programmatic stream serialization
+ *   (programmatic dependent launch): following another kernel on `stream`,
+ *   a launch may start its prologue before that kernel finishes, and waits
+ *   for its completion (griddepcontrol.wait) before touching any tensor, so
+ *   stream order is preserved for every caller-visible byte.  Stream capture
+ *   records the launches as programmatic graph edges.  The environment
+ *   variable LMBP_PDL=0, read once per process, launches them plainly.
  * State.  No global mutable state (constants only): reentrant across host
  *   threads, streams and devices.  Deterministic: no atomics, fixed
  *   reduction order, so results are bitwise identical run to run.
