@@ -830,6 +830,9 @@ template <typename K, typename... Args>
 static void launch_rows(K kernel, int64_t rows, int rows_per_block, int threads, cudaStream_t s, int occ,
                         bool persistent, Args... args) {
   const int64_t want = (rows + rows_per_block - 1) / rows_per_block;
+#ifdef LMBP_NORM_NO_PERSIST  // tuning knob (tools/gpu_stream_ab.sh): warp teams launch every CTA too
+  persistent = false;
+#endif
   const int64_t cap = (rows_per_block == 1 || !persistent) ? (int64_t)0x7fffffff : (int64_t)sm_count() * occ;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
   launch_k(kernel, grid, threads, 0, s, args...);
