@@ -337,7 +337,7 @@ static cudaError_t act_bwd_t(const void *dy, const uint8_t *codes, void *dx, int
     const int64_t want = cdiv(nvec, (int64_t)kActThreads * kActUnroll);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * occ));
     launch_k(kern, grid, kActThreads, 0, s, reinterpret_cast<const uint4 *>(dy), codes, reinterpret_cast<uint4 *>(dx),
-                                      nvec, n);
+             nvec, n);
   } else {
     auto kern = act_bwd_scalar<T, A>;
     static const int occ = occupancy(kern, kActThreads);

@@ -625,9 +625,9 @@ static cudaError_t launch_row_tma_v(const RowTmaPlan &rp, const void *a, const v
   const int64_t units = (rows + LMBP_ROW_UNIT - 1) / LMBP_ROW_UNIT;
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
   launch_k(kern, (int)units, (rp.warps + 1) * 32, rp.smem, s, reinterpret_cast<const uint4 *>(a),
-                                                        reinterpret_cast<const uint4 *>(b), rstd_in,
-                                                        reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec,
-                                                        (int)cols, eps, rp.stages);
+           reinterpret_cast<const uint4 *>(b), rstd_in,
+           reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec,
+           (int)cols, eps, rp.stages);
   return cudaGetLastError();
 }
 
@@ -691,8 +691,8 @@ static cudaError_t launch_norm_tma(const TmaPlan &tp, const void *a, const void 
   const int grid = rpw > 0 ? (int)std::max<int64_t>(1, (rows + (int64_t)tp.warps * rpw - 1) / ((int64_t)tp.warps * rpw))
                            : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
   launch_k(kern, grid, threads, tp.smem, s, reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), rstd_in,
-                                      reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec, (int)cols, eps, tp.stages,
-                                      rpw);
+           reinterpret_cast<uint4 *>(out), rstd_out, rows, nvec, (int)cols, eps, tp.stages,
+           rpw);
   return cudaGetLastError();
 }
 

@@ -358,7 +358,7 @@ cudaError_t bwd_mixed_t(const void *dy, const void *y, const float *rstd, float 
   } else {
     const int grid = (int)std::min<int64_t>(rows, (int64_t)sm_count() * 8);
     launch_k(norm_bwd_mixed_scalar<TO, NORM>, grid, 256, 0, s, reinterpret_cast<const TO *>(dy),
-                                                         reinterpret_cast<const TO *>(y), rstd, dx, rows, cols);
+             reinterpret_cast<const TO *>(y), rstd, dx, rows, cols);
   }
   return cudaGetLastError();
 }

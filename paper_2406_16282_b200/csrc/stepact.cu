@@ -485,7 +485,7 @@ static cudaError_t stepact_fwd_t(const void *x, void *y, uint8_t *codes, int64_t
     }
   }
   launch_k(stepact_fwd_k<T, A, kPrecise, K>, step_grid(n / 8), 256, 0, s, reinterpret_cast<const T *>(x),
-                                                                     reinterpret_cast<T *>(y), codes, n, tab, vec);
+           reinterpret_cast<T *>(y), codes, n, tab, vec);
   return cudaGetLastError();
 }
 
@@ -506,7 +506,7 @@ static cudaError_t stepact_bwd_t(const void *dy, const uint8_t *codes, void *dx,
     }
   }
   launch_k(stepact_bwd_k<T, K>, step_grid(n / 8), 256, 0, s, reinterpret_cast<const T *>(dy), codes,
-                                                        reinterpret_cast<T *>(dx), n, tab, vec);
+           reinterpret_cast<T *>(dx), n, tab, vec);
   return cudaGetLastError();
 }
 

@@ -180,9 +180,9 @@ static cudaError_t swiglu_fwd_t(const void *g, const void *u, void *h, void *a, 
     p.n = n;
     return launch_ew<SwiGluFwdOp<T, kPrecise>>(p, s);
   }
-  launch_k(swiglu_fwd_scalar<T, kPrecise>, scalar_grid((n + 3) / 4), 256, 0, s, 
-      reinterpret_cast<const T *>(g), reinterpret_cast<const T *>(u), reinterpret_cast<T *>(h),
-      reinterpret_cast<T *>(a), codes, n);
+  launch_k(swiglu_fwd_scalar<T, kPrecise>, scalar_grid((n + 3) / 4), 256, 0, s,
+           reinterpret_cast<const T *>(g), reinterpret_cast<const T *>(u), reinterpret_cast<T *>(h),
+           reinterpret_cast<T *>(a), codes, n);
   return cudaGetLastError();
 }
 
@@ -203,8 +203,8 @@ static cudaError_t swiglu_bwd_t(const void *dh, const void *u, const void *a, co
     return launch_ew<SwiGluBwdOp<T>>(p, s);
   }
   launch_k(swiglu_bwd_scalar<T>, scalar_grid(n), 256, 0, s, reinterpret_cast<const T *>(dh), reinterpret_cast<const T *>(u),
-                                                       reinterpret_cast<const T *>(a), codes, reinterpret_cast<T *>(dg),
-                                                       reinterpret_cast<T *>(du), n);
+           reinterpret_cast<const T *>(a), codes, reinterpret_cast<T *>(dg),
+           reinterpret_cast<T *>(du), n);
   return cudaGetLastError();
 }
 
