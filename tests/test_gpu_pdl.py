@@ -145,3 +145,33 @@ def test_pdl_off_gives_same_bytes(tmp_path):
         outs.append(np.load(path))
     for k in outs[0].files:
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+def test_pdl_honours_cross_stream_event():
+    """Stream A: our kernel, then a wait on an event of stream B, then our
+    kernel reading what B wrote.  The second launch follows a kernel on A, but
+    the event is a dependency too: it must see B's bytes, however long B
+    takes (B is made slow: many large copies before the write that matters)."""
+    R, F = 64, 3072
+    a, b = torch.cuda.Stream(DEV), torch.cuda.Stream(DEV)
+    x1 = synth.act_input(R, F, "bf16", mode="coverage").to(DEV)
+    new = synth.act_input(R, F, "bf16", mode="coverage", row_start=R).to(DEV)
+    big_src = torch.ones(64 << 20, dtype=torch.float32, device=DEV)
+    big_dst = torch.empty_like(big_src)
+    y_ref, c_ref = P.regelu2_fwd(new)
+    torch.cuda.synchronize()
+    for trial in range(5):
+        x2 = torch.zeros_like(new)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(b):
+            for _ in range(8):                    # ~2 GB of copies: B finishes long after A's first kernel
+                big_dst.copy_(big_src)
+            x2.copy_(new)
+            ev = torch.cuda.Event()
+            ev.record(b)
+        with torch.cuda.stream(a):
+            P.regelu2_fwd(x1)
+            a.wait_event(ev)
+            y2, c2 = P.regelu2_fwd(x2)
+        torch.cuda.synchronize()
+        assert torch.equal(y2.view(torch.int16), y_ref.view(torch.int16)) and torch.equal(c2, c_ref), trial
