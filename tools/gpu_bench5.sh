@@ -15,6 +15,9 @@ v = [d["value"] for d in vals]
 print(json.dumps({"runs": v, "median": statistics.median(v), "min": min(v), "max": max(v),
                   "act_fwd_us": [d["kernels"]["act_fwd"]["us"] for d in vals],
                   "frac": [d["roofline"]["frac"] for d in vals],
-                  "e2e": [d["e2e"]["value"] for d in vals], "clocks": [d["clocks"]["sm_mhz"] for d in vals]}))
+                  "e2e": [d["e2e"]["value"] for d in vals], "clocks": [d["clocks"]["sm_mhz"] for d in vals],
+                  "stream": [d["stream"]["value"] for d in vals],
+                  "graph": [d["stream"]["graph"]["value"] for d in vals],
+                  "graph_act_fwd_frac": [d["stream"]["graph"]["kernels"]["act_fwd"]["frac"] for d in vals]}))
 PY
 cat gpurun_out/bench5_wall.txt
