@@ -63,6 +63,50 @@ __device__ __forceinline__ float2 team_sum2(float2 v, float2 *buf) {
   }
 }
 
+// Row blocks of the warp-team kernels scheduled by cluster launch control:
+// the grid has one CTA per block of `teams` rows, and a running CTA takes
+// over the blocks of CTAs that have not started yet (hardware work stealing,
+// as in ew_pipeline.cuh).  Unlike a persistent grid-stride loop, a CTA that
+// starts late -- e.g. under programmatic dependent launch, once the previous
+// kernel's CTAs have left its SM -- simply ends up with fewer blocks.
+#ifndef LMBP_NORM_NO_CLC
+constexpr bool kNormClc = true;
+#else
+constexpr bool kNormClc = false;  // tuning knob: persistent grid-stride warp teams
+#endif
+#ifdef LMBP_NORM_FWD_CLC
+constexpr bool kNormFwdClc = kNormClc;
+#else
+constexpr bool kNormFwdClc = false;  // the forward keeps the persistent grid (see fwd_v)
+#endif
+template <typename F>
+__device__ __forceinline__ void clc_row_blocks(int64_t rows, int teams, int team_id, F &&body) {
+  __shared__ __align__(16) uint4 resp;
+  __shared__ uint64_t bar;
+  __shared__ int next[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int64_t blk = blockIdx.x;
+  for (uint32_t ph = 0;; ph ^= 1u) {
+    if (threadIdx.x == 0) {  // ask for the next block now; the answer arrives while this one runs
+      mbar_arrive_expect_tx(&bar, 16);
+      clc_try_cancel(&resp, &bar);
+    }
+    const int64_t row = blk * teams + team_id;
+    if (row < rows) body(row);
+    if (threadIdx.x == 0) {
+      mbar_wait(&bar, ph);
+      next[ph] = clc_query(&resp);
+    }
+    __syncthreads();
+    blk = next[ph];  // next[ph ^ 1] is written only after the next barrier: no race
+    if (blk < 0) break;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Forward, vector path.
 // ---------------------------------------------------------------------------
@@ -79,8 +123,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+  auto body = [&](int64_t row, int it) {
     const uint4 *xr = x + row * nvec;
     uint4 raw[V];
 #pragma unroll
@@ -138,6 +181,13 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_vec(const uint
       }
     }
     if (tid == 0) rstd[row] = r;
+  };
+  if constexpr (kWarpTeam && V <= 4 && kNormFwdClc) {
+    clc_row_blocks(rows, teams, team_id, [&](int64_t row) { body(row, 0); });
+  } else {
+    int it = 0;
+    for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it)
+      body(row, it);
   }
 }
 
@@ -156,8 +206,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+  auto body = [&](int64_t row, int it) {
     const uint4 *gr = dy + row * nvec;
     const uint4 *yr = y + row * nvec;
     const float r = rstd[row];
@@ -204,6 +253,13 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_vec(const uint
         st_stream(dr + vi, Vec<T>::pack(g));
       }
     }
+  };
+  if constexpr (kWarpTeam && V <= 4 && kNormClc) {
+    clc_row_blocks(rows, teams, team_id, [&](int64_t row) { body(row, 0); });
+  } else {
+    int it = 0;
+    for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it)
+      body(row, it);
   }
 }
 
@@ -844,7 +900,7 @@ static void fwd_v(const RowPlan &p, const void *x, void *y, float *rstd, int64_t
   auto k = norm_fwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
   const int occ = occupancy_of<norm_fwd_vec<T, NORM, V, W>>(threads);
-  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, V <= 4, reinterpret_cast<const uint4 *>(x),
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, V <= 4 && !(W && kNormFwdClc), reinterpret_cast<const uint4 *>(x),
               reinterpret_cast<uint4 *>(y), rstd, rows, p.nvec, (int)cols, eps);
 }
 
@@ -854,7 +910,7 @@ static void bwd_v(const RowPlan &p, const void *dy, const void *y, const float *
   auto k = norm_bwd_vec<T, NORM, V, W>;
   const int threads = W ? 256 : p.team;
   const int occ = occupancy_of<norm_bwd_vec<T, NORM, V, W>>(threads);
-  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, true, reinterpret_cast<const uint4 *>(dy),
+  launch_rows(k, rows, W ? threads / 32 : 1, threads, s, occ, !(W && V <= 4 && kNormClc), reinterpret_cast<const uint4 *>(dy),
               reinterpret_cast<const uint4 *>(y), rstd, reinterpret_cast<uint4 *>(dx), rows, p.nvec, (int)cols);
 }
 
