@@ -990,6 +990,12 @@ def main(argv=None):
     graph_ms = sw.timed_graph(sw.step, 2, args.steps, args.warmup, world)
     graph_kms = {k: sw.timed_graph(lambda i, k=k: sw.launch[k](i & 1), 8, args.steps, args.warmup, world)
                  / args.steps for k in KERNELS}
+    # context for the in-stream fractions: torch's copy of the activation
+    # tensor back to back under the same protocol (two src / dst sets)
+    cdst = [torch.empty_like(w.x), torch.empty_like(w.x)]
+    copy_ms = sw.timed_graph(lambda i: cdst[i & 1].copy_(sw.x[i & 1]), 8, args.steps, args.warmup, world) / args.steps
+    copy_gbs = 2 * w.x.numel() * w.x.element_size() / (copy_ms / 1e3) / 1e9
+    del cdst
     sw.free()
     del sw
 
@@ -1016,6 +1022,7 @@ def main(argv=None):
                         "frac": round(nbytes[k] / (graph_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
         "protocol": "the stream protocol's launches captured in CUDA graphs (2 steps, or 8 launches of one kernel, "
                     "per graph; PDL launches become programmatic edges) and replayed between one event pair",
+        "torch_copy_in_stream_GB/s": round(copy_gbs, 1),
     }
     stream_line = {
         "value": round(aggregate(bytes_all, [p[0] for p in sparts], args.steps), 1), "unit": "GB/s",
