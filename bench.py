@@ -519,7 +519,9 @@ def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
     tab = tables.REGELU2 if cfg["act"] == "gelu" else tables.RESILU2
     b, n = x.element_size(), x.numel()
     y, dx = torch.empty_like(x), torch.empty_like(dy)
-    x2, dy2 = x.clone(), dy.clone()
+    ns = stream_sets({"act": 2 * b * n}, torch.cuda.get_device_properties(x.device).L2_cache_size)
+    xs, dys = [x] + [x.clone() for _ in range(ns - 1)], [dy] + [dy.clone() for _ in range(ns - 1)]
+    ys, dxs = [y] + [torch.empty_like(y) for _ in range(ns - 1)], [dx] + [torch.empty_like(dx) for _ in range(ns - 1)]
     out = {}
     for k, thr, lv in ((2, tab["c"], tables.levels(tab)),
                        (3, [-3.0 + 1.0 * i for i in range(7)], [i / 7 for i in range(8)]),
@@ -542,18 +544,19 @@ def stepact_section(P, cfg, x, dy, stream, flush, sink, peak, iters=20):
             torch.cuda.synchronize()
             ts.append(sum(a.elapsed_time(c) for a, c in evs) / iters * 1e3)
         nbytes = 2 * (2 * b * n + P.codes_bytes_k(n, k))
-        # in-stream: back-to-back launches from a graph, alternating two input
-        # / code sets (each launch's inputs last touched > L2 bytes earlier)
-        codes2 = torch.empty_like(codes)
-        cs, xs, dys = (codes, codes2), (x, x2), (dy, dy2)
-        gf = graph_us(lambda i: P.stepact_fwd(xs[i & 1], tab["act"], k, thr, y=y, codes=cs[i & 1]), stream)
-        gb = graph_us(lambda i: P.stepact_bwd(dys[i & 1], cs[i & 1], k, lv, dx=dx), stream)
+        # in-stream: back-to-back launches from a graph over N buffer sets
+        # (every buffer touched again only after >= 3 x L2 bytes, bench.stream_sets)
+        cs = [codes] + [torch.empty_like(codes) for _ in range(ns - 1)]
+        gf = graph_us(lambda i: P.stepact_fwd(xs[i % ns], tab["act"], k, thr, y=ys[i % ns], codes=cs[i % ns]),
+                      stream, per_graph=ns * max(1, -(-8 // ns)))
+        gb = graph_us(lambda i: P.stepact_bwd(dys[i % ns], cs[i % ns], k, lv, dx=dxs[i % ns]), stream,
+                      per_graph=ns * max(1, -(-8 // ns)))
         out[f"k{k}"] = {"fwd_us": round(ts[0], 2), "bwd_us": round(ts[1], 2),
                         "GB/s": round(nbytes / (ts[0] + ts[1]) / 1e3, 1),
                         "frac": round(nbytes / (ts[0] + ts[1]) / 1e3 / peak, 4),
                         "graph_fwd_us": round(gf, 2), "graph_bwd_us": round(gb, 2),
                         "graph_frac": round(nbytes / (gf + gb) / 1e3 / peak, 4)}
-        del codes2
+        del cs
     return out
 
 
@@ -747,41 +750,47 @@ class Workload:
             setattr(self, k, None)
 
 
+def stream_sets(nbytes: dict, l2: int, cap: int = 256) -> int:
+    """Buffer sets for the in-stream protocols: enough that every buffer --
+    input or output -- is touched again only after >= 3 x L2 bytes of other
+    traffic, even when a single kernel runs back to back with itself (the
+    smallest kernel decides), so neither a read nor a rewrite of a still-dirty
+    line is served by L2."""
+    return int(max(2, min(cap, -(-3 * l2 // max(1, min(nbytes.values()))) + 1)))
+
+
 class StreamWorkload:
     """The step as a training stream runs it: the four launches back to back
     on one stream, no flush and no event between them, so each kernel's launch
     and prologue overlap the previous one's drain (programmatic dependent
-    launch, csrc/common.cuh).  Two buffer sets: step s runs the forwards on
-    set s % 2 and the backwards on set (s + 1) % 2, consuming the codes, y and
-    rstd that the forwards wrote one step earlier -- every kernel's inputs
-    were last touched at least a whole step (> 2 x L2 bytes at every config)
-    before, so nothing is served from L2 that training would not also find
-    cold.  The activation inputs of the two sets are separate copies, too."""
+    launch, csrc/common.cuh).  N complete buffer sets (inputs and outputs,
+    `stream_sets`): step s runs the forwards on set s % N and the backwards on
+    set (s + 1) % N, consuming the codes, y and rstd that set's forwards wrote
+    N - 1 steps earlier; per-kernel timings launch one kernel on sets 0, 1,
+    ... N - 1 in turn.  Every buffer is therefore last touched more than 3 x L2
+    bytes before, so nothing is served from L2 that training would not also
+    find cold (inputs) or have to write back (outputs)."""
 
-    def __init__(self, w: "Workload"):
-        self.w = w
-        clone = lambda t: t.clone()  # noqa: E731
-        self.x = [w.x, clone(w.x)]
-        self.dy = [w.dy, clone(w.dy)]
-        self.xn = [w.xn, clone(w.xn)]
-        self.gn = [w.gn, clone(w.gn)]
-        self.codes = [w.codes, torch.empty_like(w.codes)]
-        self.yn = [w.yn, torch.empty_like(w.yn)]
-        self.rstd = [w.rstd, torch.empty_like(w.rstd)]
+    def __init__(self, w: "Workload", nsets: int):
+        self.w, self.n = w, nsets
+        new = lambda t, copy: [t] + [t.clone() if copy else torch.empty_like(t) for _ in range(nsets - 1)]  # noqa
+        self.x, self.dy, self.xn, self.gn = (new(t, True) for t in (w.x, w.dy, w.xn, w.gn))
+        self.y, self.dx, self.codes, self.yn, self.rstd, self.dxn = (
+            new(t, False) for t in (w.y, w.dx, w.codes, w.yn, w.rstd, w.dxn))
         eps = w.eps
         self.s = w.stream      # the launch stream (the capture stream while a graph is recorded)
         self.launch = {
             "norm_fwd": lambda a: w.norm_fwd(self.xn[a], eps, y=self.yn[a], rstd=self.rstd[a], stream=self.s),
-            "act_fwd": lambda a: w.act_fwd(self.x[a], y=w.y, codes=self.codes[a], stream=self.s),
-            "act_bwd": lambda a: w.act_bwd(self.dy[a], self.codes[a], dx=w.dx, stream=self.s),
-            "norm_bwd": lambda a: w.norm_bwd(self.gn[a], self.yn[a], self.rstd[a], dx=w.dxn, stream=self.s),
+            "act_fwd": lambda a: w.act_fwd(self.x[a], y=self.y[a], codes=self.codes[a], stream=self.s),
+            "act_bwd": lambda a: w.act_bwd(self.dy[a], self.codes[a], dx=self.dx[a], stream=self.s),
+            "norm_bwd": lambda a: w.norm_bwd(self.gn[a], self.yn[a], self.rstd[a], dx=self.dxn[a], stream=self.s),
         }
-        for a in (0, 1):  # both sets hold a forward's outputs before the first backward reads them
+        for a in range(nsets):  # every set holds a forward's outputs before the first backward reads them
             self.launch["norm_fwd"](a)
             self.launch["act_fwd"](a)
 
     def step(self, s):
-        a, b = s & 1, (s + 1) & 1
+        a, b = s % self.n, (s + 1) % self.n
         self.launch["norm_fwd"](a)
         self.launch["act_fwd"](a)
         self.launch["act_bwd"](b)
@@ -811,9 +820,9 @@ class StreamWorkload:
         return self._time(self.step, steps, warmup, world)
 
     def graph(self, body, n):
-        """A CUDA graph of body(0) .. body(n - 1) (n even: both buffer sets),
-        recorded from the same launches (PDL launches become programmatic
-        edges), so replaying it costs one host call per n launches."""
+        """A CUDA graph of body(0) .. body(n - 1), recorded from the same
+        launches (PDL launches become programmatic edges), so replaying it
+        costs one host call per n launches."""
         g = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream(self.w.dev)
         cs.wait_stream(self.w.stream)
@@ -825,24 +834,27 @@ class StreamWorkload:
         self.w.stream.wait_stream(cs)
         return g
 
-    def timed_graph(self, body, per_graph, total, warmup, world):
-        """ms for `total` units (launches or steps) replayed from a graph of
-        `per_graph` units, between one event pair."""
+    def timed_graph(self, body, per_graph, units, warmup, world):
+        """ms per unit (launch or step): a graph of `per_graph` units (a
+        multiple of the set count, so it covers every set) replayed until at
+        least `units` units have run, between one event pair."""
         g = self.graph(body, per_graph)
-        reps = max(1, total // per_graph)
+        reps = max(1, -(-units // per_graph))
         with torch.cuda.stream(self.w.stream):
             ms = self._time(lambda i: g.replay(), reps, max(1, warmup // per_graph), world)
         del g
-        return ms * total / (reps * per_graph)
+        return ms / (reps * per_graph)
+
+    def per_graph(self, at_least=8):
+        return self.n * max(1, -(-at_least // self.n))
 
     def timed_kernel(self, k, launches, warmup, world):
-        """ms for `launches` back-to-back launches of one kernel, alternating
-        the two buffer sets (its inputs last touched one launch earlier, more
-        than L2's capacity before)."""
-        return self._time(lambda i: self.launch[k](i & 1), launches, warmup, world)
+        """ms per launch for back-to-back launches of one kernel on sets 0, 1, .."""
+        return self._time(lambda i: self.launch[k](i % self.n), launches, warmup, world) / launches
 
     def free(self):
-        self.x = self.dy = self.xn = self.gn = self.codes = self.yn = self.rstd = None
+        for k in ("x", "dy", "xn", "gn", "y", "dx", "codes", "yn", "rstd", "dxn"):
+            setattr(self, k, None)
 
 
 def gather_floats(vals, world, cdev):
@@ -982,20 +994,21 @@ def main(argv=None):
     per_kernel = w.timed(flush, flush_sink, args.steps, args.warmup, world, sampler)
     clocks = sampler.stop()
 
-    sw = StreamWorkload(w)
+    nsets = stream_sets(w.nbytes, l2)
+    sw = StreamWorkload(w, nsets)
     stream_ms = sw.timed_steps(args.steps, args.warmup, world)
     t_host = sw.last_host_s
-    stream_kms = {k: sw.timed_kernel(k, args.steps, args.warmup, world) / args.steps for k in KERNELS}
+    stream_kms = {k: sw.timed_kernel(k, args.steps, args.warmup, world) for k in KERNELS}
     # the same launches replayed from CUDA graphs (no per-launch host cost)
-    graph_ms = sw.timed_graph(sw.step, 2, args.steps, args.warmup, world)
-    graph_kms = {k: sw.timed_graph(lambda i, k=k: sw.launch[k](i & 1), 8, args.steps, args.warmup, world)
-                 / args.steps for k in KERNELS}
+    pg = sw.per_graph(2)
+    graph_ms = sw.timed_graph(sw.step, pg, args.steps, args.warmup, world) * args.steps
+    graph_kms = {k: sw.timed_graph(lambda i, k=k: sw.launch[k](i % nsets), sw.per_graph(8), args.steps,
+                                   args.warmup, world) for k in KERNELS}
     # context for the in-stream fractions: torch's copy of the activation
-    # tensor back to back under the same protocol (two src / dst sets)
-    cdst = [torch.empty_like(w.x), torch.empty_like(w.x)]
-    copy_ms = sw.timed_graph(lambda i: cdst[i & 1].copy_(sw.x[i & 1]), 8, args.steps, args.warmup, world) / args.steps
+    # tensor back to back under the same protocol (the sets' x -> y)
+    copy_ms = sw.timed_graph(lambda i: sw.y[i % nsets].copy_(sw.x[i % nsets]), sw.per_graph(8), args.steps,
+                             args.warmup, world)
     copy_gbs = 2 * w.x.numel() * w.x.element_size() / (copy_ms / 1e3) / 1e9
-    del cdst
     sw.free()
     del sw
 
@@ -1020,8 +1033,8 @@ def main(argv=None):
         "kernels": {k: {"us": round(graph_kms[k] * 1e3, 2),
                         "GB/s": round(nbytes[k] / (graph_kms[k] / 1e3) / 1e9, 1),
                         "frac": round(nbytes[k] / (graph_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
-        "protocol": "the stream protocol's launches captured in CUDA graphs (2 steps, or 8 launches of one kernel, "
-                    "per graph; PDL launches become programmatic edges) and replayed between one event pair",
+        "protocol": "the stream protocol's launches captured in CUDA graphs (a whole number of passes over the "
+                    "buffer sets per graph; PDL launches become programmatic edges), replayed between one event pair",
         "torch_copy_in_stream_GB/s": round(copy_gbs, 1),
     }
     stream_line = {
@@ -1034,9 +1047,11 @@ def main(argv=None):
         "kernels": {k: {"us": round(stream_kms[k] * 1e3, 2),
                         "GB/s": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9, 1),
                         "frac": round(nbytes[k] / (stream_kms[k] / 1e3) / 1e9 / peak, 4)} for k in KERNELS},
-        "protocol": "K steps back to back between one CUDA event pair, no flush; forwards on buffer set s%2, "
-                    "backwards on set (s+1)%2 (inputs last touched a step earlier); per-kernel: K back-to-back "
-                    "launches alternating the two sets between one event pair",
+        "protocol": "K steps back to back between one CUDA event pair, no flush; N complete buffer sets (inputs "
+                    "and outputs), forwards on set s%N, backwards on set (s+1)%N, so every buffer is touched again "
+                    "only after >= 3 x L2 bytes of other traffic; per-kernel: K back-to-back launches on sets "
+                    "0, 1, .. between one event pair",
+        "buffer_sets": nsets,
     }
 
     kern = {}
