@@ -80,3 +80,16 @@ def test_shard_checksums_match_one_gpu_and_catch_a_flipped_or_moved_byte():
                 raw[j], raw[j + 1] = raw[j + 1].clone(), raw[j].clone()
             got = bench.output_checksums(_FakeWorkload(cfg, bad, r0, n), r0, r0 + n, r0)
             assert got[i] != ref[i], (name, mutate)
+
+
+def test_stream_sets_keep_every_buffer_cold():
+    """The in-stream protocols' set count: a kernel launched back to back with
+    itself over N sets touches a buffer again only after (N - 1) launches,
+    which must be >= 3 x L2 bytes for the smallest kernel of every config."""
+    l2 = 126 << 20
+    for name, cfg in synth.CONFIGS.items():
+        nb = bench.algorithmic_bytes(cfg, cfg["R"])
+        n = bench.stream_sets(nb, l2)
+        assert n >= 2
+        if n < 256:
+            assert (n - 1) * min(nb.values()) >= 3 * l2, name
