@@ -848,7 +848,10 @@ static RowPlan plan_rows(int64_t cols, const void *a, const void *b, const void 
     p.team = 32;
     p.V = (int)((nvec + 31) / 32);
   } else {
-    const int64_t want = (nvec + 3) / 4;           // aim for 4 vectors per thread
+#ifndef LMBP_NORM_VAIM
+#define LMBP_NORM_VAIM 4
+#endif
+    const int64_t want = (nvec + LMBP_NORM_VAIM - 1) / LMBP_NORM_VAIM;  // aim for 4 vectors per thread
     int64_t team = ((want + 31) / 32) * 32;
     if (team > 512) team = 512;
     p.team = (int)team;
