@@ -1185,6 +1185,9 @@ def main(argv=None):
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),
             "fraction_of_8TBs": round(value / world / NOMINAL_HBM_GBS, 4),
+            "families": {fam: {"fwd_bwd_GB/s": round((nbytes[f] + nbytes[b]) / ((kern[f]["us"] + kern[b]["us"]) / 1e6) / 1e9, 1),
+                               "frac": round((nbytes[f] + nbytes[b]) / ((kern[f]["us"] + kern[b]["us"]) / 1e6) / 1e9 / peak, 4)}
+                         for fam, f, b in (("act", "act_fwd", "act_bwd"), ("norm", "norm_fwd", "norm_bwd"))},
             "elements_per_s": round(sum(bytes_all) / step_bytes * (R * F * 2 + R * H * 2) * args.steps
                                     / (max_ms / 1e3), 1),
             "per_rank_ms": [round(m, 3) for m in ms_all],
