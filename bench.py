@@ -43,6 +43,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
+from paper_2406_16282_b200.build import build_info  # noqa: E402  (provenance only; imports no kernels)
 
 METRIC = "fwd+bwd HBM GB/s (fraction of B200 peak) and activation bytes saved per layer"
 NOMINAL_HBM_GBS = 8000.0
@@ -1181,6 +1182,7 @@ def main(argv=None):
                        "dist_backend": backend if world > 1 else None,
                        "devices": min(world, ndev)},
             "stream": stream_line,
+            "build": build_info(),
             "roofline": roofline, "rw_model": rw_model, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 4 * args.steps, "clocks": clocks, "kernels": kern,
             "fraction_of_measured_peak": round(value / world / peak, 4),

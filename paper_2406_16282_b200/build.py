@@ -16,6 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "liblmbp.so")
+LIB_INFO = os.path.join(HERE, "liblmbp.build.json")   # provenance of LIB (travels with it; not committed)
 SOURCES = ["abi.cu", "act.cu", "norm.cu", "norm_mixed.cu", "swiglu.cu", "stepact.cu", "fit.cu"]
 HEADERS = ["common.cuh", "constants.cuh", "kernels.h", "act_math.cuh", "act_lut.cuh", "ew_pipeline.cuh",
            os.path.join("..", "..", "include", "lmbp.h"), os.path.join("..", "_obj", "act_lut.inc")]
@@ -79,7 +80,53 @@ def build(force: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
+    if force or _stale(LIB_INFO, [LIB]):
+        write_build_info()
     return LIB
+
+
+def source_digest() -> str:
+    """sha256 over every file the library is compiled from (kernel sources,
+    headers, the C ABI header, the table generator), in a fixed order."""
+    import hashlib
+    h = hashlib.sha256()
+    files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS[:-2]] + \
+        [os.path.join(ROOT, "include", "lmbp.h"), os.path.join(HERE, "lut.py"), os.path.abspath(__file__)]
+    for path in files:
+        h.update(os.path.relpath(path, ROOT).encode())
+        with open(path, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def write_build_info() -> None:
+    import json
+    import time
+    try:
+        sha = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True).stdout.strip()
+        dirty = bool(subprocess.run(["git", "-C", ROOT, "status", "--porcelain", "--", "paper_2406_16282_b200/csrc",
+                                     "include"], capture_output=True, text=True).stdout.strip())
+    except OSError:
+        sha, dirty = "", None
+    nv = subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.strip().splitlines()
+    info = {"source_sha256": source_digest(), "git_head": sha or None, "sources_dirty": dirty,
+            "nvcc": nv[-1] if nv else None, "arch": "sm_100a",
+            "built_utc": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    with open(LIB_INFO, "w") as f:
+        json.dump(info, f, indent=1)
+
+
+def build_info() -> dict:
+    """LIB's recorded provenance plus whether it matches the sources present
+    now (the check a benchmark or test run reports)."""
+    import json
+    try:
+        info = json.load(open(LIB_INFO))
+    except (OSError, ValueError):
+        return {"recorded": False}
+    info["recorded"] = True
+    info["matches_sources"] = info.get("source_sha256") == source_digest()
+    return info
 
 
 def build_variant(name: str, defines, sources=None) -> str:

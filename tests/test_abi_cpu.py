@@ -250,3 +250,13 @@ def test_mixed_norm_validation_without_device_work():
         assert fn(fake, fake, fake, fake, 2, 8, S.LMBP_F32, None) == S.LMBP_ERR_DTYPE
         assert fn(fake, fake, None, fake, 2, 8, S.LMBP_BF16, None) == S.LMBP_ERR_NULLPTR
         assert fn(None, None, None, None, 0, 8, S.LMBP_F16, None) == S.LMBP_OK
+
+
+def test_library_provenance_matches_sources():
+    """build() records the sha256 of every source the library is compiled
+    from next to it (liblmbp.build.json, reported by bench.py); the library in
+    the tree was built from the sources in the tree."""
+    from paper_2406_16282_b200 import build as B
+    info = B.build_info()
+    assert info["recorded"] and info["arch"] == "sm_100a"
+    assert info["matches_sources"], "liblmbp.so is stale: rebuild with python -m paper_2406_16282_b200.build"
