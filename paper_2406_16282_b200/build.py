@@ -80,8 +80,8 @@ def build(force: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
-    if force or _stale(LIB_INFO, [LIB]):
-        write_build_info()
+    if force or _stale(LIB_INFO, [LIB]) or not build_info().get("matches_sources"):
+        write_build_info()   # (objects are rebuilt from exactly these sources above)
     return LIB
 
 
@@ -91,7 +91,7 @@ def source_digest() -> str:
     import hashlib
     h = hashlib.sha256()
     files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS[:-2]] + \
-        [os.path.join(ROOT, "include", "lmbp.h"), os.path.join(HERE, "lut.py"), os.path.abspath(__file__)]
+        [os.path.join(ROOT, "include", "lmbp.h"), os.path.join(HERE, "lut.py")]
     for path in files:
         h.update(os.path.relpath(path, ROOT).encode())
         with open(path, "rb") as f:
