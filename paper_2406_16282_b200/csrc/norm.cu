@@ -63,12 +63,6 @@ __device__ __forceinline__ float2 team_sum2(float2 v, float2 *buf) {
   }
 }
 
-// Row blocks of the warp-team kernels scheduled by cluster launch control:
-// the grid has one CTA per block of `teams` rows, and a running CTA takes
-// over the blocks of CTAs that have not started yet (hardware work stealing,
-// as in ew_pipeline.cuh).  Unlike a persistent grid-stride loop, a CTA that
-// starts late -- e.g. under programmatic dependent launch, once the previous
-// kernel's CTAs have left its SM -- simply ends up with fewer blocks.
 #ifndef LMBP_NORM_NO_CLC
 constexpr bool kNormClc = true;
 #else
@@ -79,33 +73,6 @@ constexpr bool kNormFwdClc = kNormClc;
 #else
 constexpr bool kNormFwdClc = false;  // the forward keeps the persistent grid (see fwd_v)
 #endif
-template <typename F>
-__device__ __forceinline__ void clc_row_blocks(int64_t rows, int teams, int team_id, F &&body) {
-  __shared__ __align__(16) uint4 resp;
-  __shared__ uint64_t bar;
-  __shared__ int next[2];
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int64_t blk = blockIdx.x;
-  for (uint32_t ph = 0;; ph ^= 1u) {
-    if (threadIdx.x == 0) {  // ask for the next block now; the answer arrives while this one runs
-      mbar_arrive_expect_tx(&bar, 16);
-      clc_try_cancel(&resp, &bar);
-    }
-    const int64_t row = blk * teams + team_id;
-    if (row < rows) body(row);
-    if (threadIdx.x == 0) {
-      mbar_wait(&bar, ph);
-      next[ph] = clc_query(&resp);
-    }
-    __syncthreads();
-    blk = next[ph];  // next[ph ^ 1] is written only after the next barrier: no race
-    if (blk < 0) break;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Forward, vector path.

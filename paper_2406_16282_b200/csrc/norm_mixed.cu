@@ -153,8 +153,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(cons
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
-  int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
+  auto body = [&](int64_t row, int it) {
     const uint4 *gr = dy + row * (int64_t)ngrp;
     const uint4 *yr = y + row * (int64_t)ngrp;
     const float r = rstd[row];
@@ -201,6 +200,13 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(cons
         st_stream(dr + 2 * gi + 1, Vec<float>::pack(g + 4));
       }
     }
+  };
+  if constexpr (kWarpTeam) {  // one CTA per 8-row block, work stealing (as norm.cu's backward)
+    clc_row_blocks(rows, teams, team_id, [&](int64_t row) { body(row, 0); });
+  } else {
+    int it = 0;
+    for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it)
+      body(row, it);
   }
 }
 
@@ -341,9 +347,8 @@ cudaError_t bwd_mixed_t(const void *dy, const void *y, const float *rstd, float 
   uint4 *dv = reinterpret_cast<uint4 *>(dx);
   if (p.vec && p.warp) {
     auto launch = [&](auto kern) {
-      static const int occ = occupancy_mixed(kern, 256);
-      const int64_t want = (rows + 7) / 8;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
+      const int64_t want = (rows + 7) / 8;   // every block gets a CTA; running ones steal (CLC)
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 0x7fffffff));
       launch_k(kern, grid, 256, 0, s, gv, yv, rstd, dv, rows, p.ngrp, (int)cols);
     };
     switch (p.V) {
