@@ -42,8 +42,13 @@
  *   a launch may start its prologue before that kernel finishes, and waits
  *   for its completion (griddepcontrol.wait) before touching any tensor, so
  *   stream order is preserved for every caller-visible byte.  Stream capture
- *   records the launches as programmatic graph edges.  The environment
- *   variable LMBP_PDL=0, read once per process, launches them plainly.
+ *   records the launches as programmatic graph edges.  Each kernel signals
+ *   launch_dependents at entry, so a caller's OWN kernel launched with the
+ *   PDL attribute right after one of ours may start early and must call
+ *   cudaGridDependencySynchronize() before reading our outputs (as PDL
+ *   requires of any dependent); plain launches are unaffected.  The
+ *   environment variable LMBP_PDL=0, read once per process, launches ours
+ *   plainly.
  * State.  No global mutable state (constants only): reentrant across host
  *   threads, streams and devices.  Deterministic: no atomics, fixed
  *   reduction order, so results are bitwise identical run to run.
