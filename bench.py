@@ -443,9 +443,22 @@ def swiglu_section(P, cfg, gate, up, stream, flush, sink, args, iters=20):
     bf, bb = (4 * b * n + (n + 3) // 4), (5 * b * n + (n + 3) // 4)
     tf, tb = timeit(fused["fwd"]), timeit(fused["bwd"])
     uf, ub = timeit(unfused_fwd), timeit(unfused_bwd)
+    # in-stream: back-to-back fused launches from a graph over N complete buffer sets
+    ns = stream_sets({"fwd": bf}, torch.cuda.get_device_properties(gate.device).L2_cache_size)
+    more = lambda t, copy: [t] + [t.clone() if copy else torch.empty_like(t) for _ in range(ns - 1)]  # noqa: E731
+    G, Uu, DH, H, A, C, DG, DU = (more(gate, True), more(up, True), more(dh, True), more(h, False), more(a, False),
+                                  more(codes, False), more(dg, False), more(du, False))
+    pg = ns * max(1, -(-8 // ns))
+    gf = graph_us(lambda i: P.reswiglu2_fwd(G[i % ns], Uu[i % ns], h=H[i % ns], a=A[i % ns], codes=C[i % ns]),
+                  stream, per_graph=pg)
+    gb = graph_us(lambda i: P.reswiglu2_bwd(DH[i % ns], Uu[i % ns], A[i % ns], C[i % ns], dgate=DG[i % ns],
+                                            dup=DU[i % ns]), stream, per_graph=pg)
+    del G, Uu, DH, H, A, C, DG, DU
     return {"shape": list(gate.shape), "fused_fwd_us": round(tf, 2), "fused_bwd_us": round(tb, 2),
             "fused_GB/s": round((bf + bb) / (tf + tb) / 1e3, 1),
             "fused_frac": round((bf + bb) / (tf + tb) / 1e3 / measured_hbm_peak()[0], 4),
+            "graph_fwd_us": round(gf, 2), "graph_bwd_us": round(gb, 2),
+            "graph_frac": round((bf + bb) / (gf + gb) / 1e3 / measured_hbm_peak()[0], 4),
             "unfused_fwd_us": round(uf, 2), "unfused_bwd_us": round(ub, 2),
             "speedup_fwd_bwd": round((uf + ub) / (tf + tb), 3),
             "algorithmic_bytes": {"fwd": bf, "bwd": bb},
