@@ -15,8 +15,8 @@ between).  value = algorithmic bytes of all ranks / max-over-ranks device time.
 The `stream` key times the same step the way a training stream runs it: K
 steps back to back between one event pair, no flush, consecutive kernels
 overlapped by programmatic dependent launch, the backwards of step s reading
-what the forwards of step s-1 wrote (two buffer sets, so every input was last
-touched more than L2's capacity earlier).  DESIGN.md 5.10 and 6.
+what the forwards of an earlier step wrote (N complete buffer sets, so every
+buffer is touched again only after >= 3 x L2 bytes).  DESIGN.md 5.10 and 6.
 
 Multi-GPU: one process per GPU; every rank processes its own batch of the
 configured shape (weak scaling, data-parallel, no collective on the data path);
