@@ -910,7 +910,7 @@ def output_checksums(w, r0, r1, base_row):
         for c in range(0, raw.numel(), 1 << 26):   # 64 MB chunks bound the int64 temporaries
             b = raw[c:c + (1 << 26)].to(torch.int64)
             pos = torch.arange(p0 + c, p0 + c + b.numel(), device=b.device, dtype=torch.int64)
-            acc = (acc + int((((b + 1) * ((pos * 2654435761) % 1000003 + 1)) % M).sum().item())) % M
+            acc = (acc + int((((b + 1) * ((pos % 1000003) * 2654435761 % 1000003 + 1)) % M).sum().item())) % M
         out.append(float(acc))                      # < 2^31: exact in the float64 gather
     return out
 
