@@ -54,6 +54,26 @@ __device__ __forceinline__ void st_stream(uint4 *p, const uint4 &v) {
 #endif
 }
 
+// 32 contiguous bytes per thread in one 256-bit access (sm_100 .v8.b32): a
+// warp instruction then covers 1 KB of whole sectors, where two 16-byte
+// accesses at a 32-byte stride each touch every sector half.  p must be
+// 32-byte aligned.
+#ifndef LMBP_NO_V8
+constexpr bool kUseV8 = true;
+#else
+constexpr bool kUseV8 = false;  // tuning knob: pairs of 16-byte accesses instead
+#endif
+__device__ __forceinline__ void st_stream32(uint4 *p, const uint4 &a, const uint4 &b) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+__device__ __forceinline__ void ld_stream32(const uint4 *p, uint4 &a, uint4 &b) {
+  asm volatile("ld.global.L1::no_allocate.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 // ---------------------------------------------------------------------------
 // Element conversions (round-to-nearest-even, no FTZ).
 // ---------------------------------------------------------------------------

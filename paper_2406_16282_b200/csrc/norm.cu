@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t row_bytes = (size_t)nvec * 16;
   const size_t stage_bytes = row_bytes * NIN;
+  const bool out32 = kUseV8 && ((uintptr_t)out & 31u) == 0;  // fp32 rows are 32 B multiples: whole 256-bit stores
   // layout: stages | clc response (16 B) | full[S] empty[S] clc_bar | slot[S] | red | rslot[S]
   uint4 *clc_resp = reinterpret_cast<uint4 *>(smem + (size_t)stages * stage_bytes);  // 16-byte aligned
   uint64_t *full = reinterpret_cast<uint64_t *>(clc_resp + 1);
@@ -585,8 +586,12 @@ __global__ void __launch_bounds__(544) norm_row_tma(const uint4 *a, const uint4 
           }
           if constexpr (kF32Out) {
             uint4 *o32 = out + row * (int64_t)nvec * 2;
-            st_stream(o32 + 2 * vi, Vec<float>::pack(g));
-            st_stream(o32 + 2 * vi + 1, Vec<float>::pack(g + 4));
+            if (out32) {
+              st_stream32(o32 + 2 * vi, Vec<float>::pack(g), Vec<float>::pack(g + 4));
+            } else {
+              st_stream(o32 + 2 * vi, Vec<float>::pack(g));
+              st_stream(o32 + 2 * vi + 1, Vec<float>::pack(g + 4));
+            }
           } else {
             st_stream(orow + vi, Vec<T>::pack(g));
           }

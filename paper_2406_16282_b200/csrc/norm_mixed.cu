@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_mixed_vec(cons
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
+  const bool x32 = kUseV8 && ((uintptr_t)x & 31u) == 0;  // fp32 rows are 32 B multiples: whole 256-bit loads
   int it = 0;
   for (int64_t row = (int64_t)blockIdx.x * teams + team_id; row < rows; row += (int64_t)gridDim.x * teams, ++it) {
     const uint4 *xr = x + row * (int64_t)ngrp * 2;
@@ -84,8 +85,12 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_fwd_mixed_vec(cons
     for (int j = 0; j < V; ++j) {
       const int gi = j * team + tid;
       if (gi < ngrp) {
-        ra[j] = ld_stream(xr + 2 * gi);
-        rb[j] = ld_stream(xr + 2 * gi + 1);
+        if (x32) {
+          ld_stream32(xr + 2 * gi, ra[j], rb[j]);
+        } else {
+          ra[j] = ld_stream(xr + 2 * gi);
+          rb[j] = ld_stream(xr + 2 * gi + 1);
+        }
       } else {
         ra[j] = rb[j] = make_uint4(0u, 0u, 0u, 0u);
       }
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(cons
   const int teams = kWarpTeam ? (int)(blockDim.x >> 5) : 1;
   const int team_id = kWarpTeam ? (int)(threadIdx.x >> 5) : 0;
   const float fcols = (float)cols;
+  const bool dx32 = kUseV8 && ((uintptr_t)dx & 31u) == 0;
   auto body = [&](int64_t row, int it) {
     const uint4 *gr = dy + row * (int64_t)ngrp;
     const uint4 *yr = y + row * (int64_t)ngrp;
@@ -196,8 +202,12 @@ __global__ void __launch_bounds__(kWarpTeam ? 256 : 512) norm_bwd_mixed_vec(cons
           const float c = NORM == kNormLN ? __fsub_rn(g[k], m1) : g[k];
           g[k] = __fmul_rn(r, fmaf(-h[k], m2, c));
         }
-        st_stream(dr + 2 * gi, Vec<float>::pack(g));
-        st_stream(dr + 2 * gi + 1, Vec<float>::pack(g + 4));
+        if (dx32) {
+          st_stream32(dr + 2 * gi, Vec<float>::pack(g), Vec<float>::pack(g + 4));
+        } else {
+          st_stream(dr + 2 * gi, Vec<float>::pack(g));
+          st_stream(dr + 2 * gi + 1, Vec<float>::pack(g + 4));
+        }
       }
     }
   };

@@ -66,6 +66,11 @@ __device__ __forceinline__ void load8(const T *p, int64_t g, bool vec, float *f)
   if (vec) {
     if constexpr (Traits<T>::kVec == 8) {
       Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + g), f);
+    } else if (kUseV8 && ((uintptr_t)p & 31u) == 0) {  // 8 fp32 = one 256-bit access
+      uint4 a, b;
+      ld_stream32(reinterpret_cast<const uint4 *>(p) + 2 * g, a, b);
+      Vec<T>::unpack(a, f);
+      Vec<T>::unpack(b, f + 4);
     } else {
       Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + 2 * g), f);
       Vec<T>::unpack(ld_stream(reinterpret_cast<const uint4 *>(p) + 2 * g + 1), f + 4);
@@ -81,6 +86,8 @@ __device__ __forceinline__ void store8(T *p, int64_t g, bool vec, const float *f
   if (vec) {
     if constexpr (Traits<T>::kVec == 8) {
       st_stream(reinterpret_cast<uint4 *>(p) + g, Vec<T>::pack(f));
+    } else if (kUseV8 && ((uintptr_t)p & 31u) == 0) {
+      st_stream32(reinterpret_cast<uint4 *>(p) + 2 * g, Vec<T>::pack(f), Vec<T>::pack(f + 4));
     } else {
       st_stream(reinterpret_cast<uint4 *>(p) + 2 * g, Vec<T>::pack(f));
       st_stream(reinterpret_cast<uint4 *>(p) + 2 * g + 1, Vec<T>::pack(f + 4));
