@@ -374,7 +374,8 @@ __device__ __forceinline__ void clc_row_blocks(int64_t rows, int teams, int team
       next[ph] = clc_query(&resp);
     }
     __syncthreads();
-    blk = next[ph];  // next[ph ^ 1] is written only after the next barrier: no race
+    blk = next[ph];  // thread 0 rewrites next[ph] two iterations on, after a barrier every thread
+                     // reaches only once it has read it here
     if (blk < 0) break;
   }
 }
