@@ -1101,7 +1101,11 @@ def main(argv=None):
                 "traffic_note": "ncu dram read+write per launch; DRAM writes still dirty in L2 at kernel end are "
                                 "not counted, so l2_write_bytes (every byte the SMs stored, from the same capture) "
                                 "is the write side to compare with the algorithmic bytes",
-                "l2_write_bytes": l2w}
+                "l2_write_bytes": l2w,
+                # the same kernel back to back in a stream (graph replay, N buffer sets, PDL): its prologue and
+                # launch hidden, the previous launch's dirty L2 lines charged (DESIGN 5.10, 6)
+                "in_stream": {"achieved": graph_line["kernels"][dom]["GB/s"],
+                              "frac": graph_line["kernels"][dom]["frac"], "us": graph_line["kernels"][dom]["us"]}}
 
     # e2e through the public API with host buffers: H2D inputs, 4 kernels, D2H results
     e2e = None
